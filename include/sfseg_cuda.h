@@ -1,0 +1,208 @@
+/*
+ * sfseg_cuda.h — C ABI of the B200 (sm_100a) SFSeg power-iteration library.
+ *
+ * This is the drop-in boundary for the reference's engine (proj/include/sfseg/
+ * engine.hpp). Every entry point takes plain pointers and sizes; no C++, torch
+ * or CUDA types cross it. The C++ shim in
+ * paper_1907_02731_b200/csrc/engine_shim.cpp re-exports these calls as the
+ * seven symbols of the reference's engine.o (sfseg::SfsegConfig::validate,
+ * sfseg_step_channel, sfseg_step, normalize_l2, project_binary,
+ * threshold_final, run), so a reference build links the GPU engine instead of
+ * engine.cpp without touching its headers or callers.
+ *
+ * Volumes are dense float32, frame-major then row-major:
+ *   index(t, y, x) = (t * H + y) * W + x        (volume.hpp:32-36)
+ * Pointers flagged SFSEG_MEM_HOST are ordinary (pageable or pinned) host
+ * memory; SFSEG_MEM_DEVICE pointers live on the context's device in the same
+ * dense layout. Internally the context keeps a row-pitched copy in HBM.
+ *
+ * Error behaviour: every call returns an SFSEG_* status. The numeric codes map
+ * 1:1 onto the reference's exception types (errors.hpp:17-68); the message of
+ * the last failure on the calling thread is available from sfseg_last_error().
+ * There is no CPU fallback: without a usable sm_100 device every compute call
+ * fails with SFSEG_ERR_CUDA.
+ */
+#ifndef SFSEG_CUDA_H
+#define SFSEG_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFSEG_CUDA_ABI_VERSION 1
+
+/* Status codes. Each names the sfseg:: exception the C++ shim rethrows. */
+enum sfseg_status {
+    SFSEG_OK = 0,
+    SFSEG_ERR_PARAMETER = 1,  /* ParameterError          (engine.cpp:21-42, 144-145) */
+    SFSEG_ERR_SHAPE = 2,      /* ShapeError              (engine.cpp:124-127, 263, 271-274) */
+    SFSEG_ERR_VALIDATION = 3, /* ValidationError         (volume.cpp:72-93, engine.cpp:266) */
+    SFSEG_ERR_DEGENERATE = 4, /* DegenerateSolutionError (engine.cpp:174-175) */
+    SFSEG_ERR_CAPACITY = 5,   /* CapacityError           (device memory exhausted) */
+    SFSEG_ERR_CUDA = 6,       /* Error                   (CUDA runtime/driver failure) */
+    SFSEG_ERR_STATE = 7       /* Error                   (API misuse, e.g. solve before load) */
+};
+
+/* Arithmetic contract of the stencil kernels.
+ *  EXACT: every product and sum rounded separately in the reference's order
+ *         (conv3d.cpp:80-167, engine.cpp:92-119; the reference is built without
+ *         FMA contraction). Outputs of a step are bit-identical to the CPU
+ *         reference; the L2 norm differs only in the fp64 summation order.
+ *  FAST:  fused multiply-adds and the cheaper y->x->t pass order; agrees with
+ *         the reference within the north-star tolerance (max abs 1e-4,
+ *         cosine >= 1-1e-6 after normalisation). */
+enum sfseg_arith { SFSEG_ARITH_EXACT = 0, SFSEG_ARITH_FAST = 1 };
+
+enum sfseg_mem { SFSEG_MEM_HOST = 0, SFSEG_MEM_DEVICE = 1 };
+
+/* Mirrors sfseg::SfsegConfig (engine.hpp:22-57) and KernelConfig
+ * (conv3d.hpp:20-23). Axis order of radii/sigmas is (t, y, x). */
+typedef struct sfseg_params {
+    double alpha;
+    double p;
+    int32_t radii[3];
+    double sigmas[3];
+    int32_t iterations;
+    int32_t temporal_window;
+    int32_t binarize_start;
+    double sigmoid_slope0;
+    double slope_growth;
+    double threshold_frac;
+    double final_threshold;
+    int32_t allow_negative_affinity;
+    int32_t arith; /* enum sfseg_arith */
+} sfseg_params;
+
+/* Per-iteration record (metrics.hpp:34-40). angle/iou are NaN when the
+ * corresponding reference / ground truth was not supplied. */
+typedef struct sfseg_iter_record {
+    int32_t iter;
+    double l2_norm_pre_normalize;
+    double angle_deg;
+    double iou;
+    double wall_time_s;
+} sfseg_iter_record;
+
+/* Device timing of the last solve (CUDA events on the context stream). */
+typedef struct sfseg_timing {
+    double solve_ms;        /* whole iteration loop, first launch to last */
+    double step_kernel_ms;  /* sum of the fused stencil kernel launches */
+    int32_t step_launches;  /* number of fused stencil kernel launches */
+    int32_t total_launches; /* every kernel this library launched in the loop */
+    double bytes_per_launch; /* algorithmic HBM bytes of one stencil launch */
+} sfseg_timing;
+
+/* ---- configuration ------------------------------------------------------ */
+
+/* Defaults of SfsegConfig / KernelConfig (engine.hpp:23-49, conv3d.hpp:21-22). */
+void sfseg_params_default(sfseg_params* p);
+
+/* SfsegConfig::validate (engine.cpp:21-42). SFSEG_OK or SFSEG_ERR_PARAMETER. */
+int sfseg_params_validate(const sfseg_params* p);
+
+/* Kernel taps exactly as make_gaussian_kernel (conv3d.cpp:23-58): fp64 raw
+ * Gaussian taps, product mass folded into taps_t. Each out array must hold
+ * 2*radius+1 doubles. */
+int sfseg_make_kernel(const int32_t radii[3], const double sigmas[3], double* taps_t,
+                      double* taps_y, double* taps_x);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* sfseg_last_error(void);
+
+/* Library build information (arch, version) as a static string. */
+const char* sfseg_build_info(void);
+
+/* ---- context ------------------------------------------------------------ */
+
+typedef struct sfseg_ctx sfseg_ctx;
+
+/* Creates a context bound to CUDA device `device` with its own stream. */
+int sfseg_ctx_create(int device, sfseg_ctx** out);
+int sfseg_ctx_destroy(sfseg_ctx* ctx);
+/* Enables per-launch CUDA-event timing of the stencil kernel (bench only). */
+int sfseg_ctx_set_timing(sfseg_ctx* ctx, int enabled);
+int sfseg_ctx_get_timing(const sfseg_ctx* ctx, sfseg_timing* out);
+/* Blocks until the context stream is idle. */
+int sfseg_ctx_synchronize(sfseg_ctx* ctx);
+
+/* ---- resident problem (run(), engine.cpp:247-348) ----------------------- */
+
+/* Uploads S (unary) and C pairwise channels, validates them on the device
+ * (FeatureSet::validate, volume.cpp:72-93) and keeps them resident. x0 is
+ * optional (NULL = start from S, engine.cpp:267-270). */
+int sfseg_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+               int32_t channels, const float* unary, const float* const* pairwise,
+               const float* x0, int32_t mem);
+
+/* Runs iterations first_iter..last_iter (1-based, inclusive) of Algorithm 1
+ * on the resident problem. first_iter == 1 restarts from S or x0; otherwise
+ * the call continues from the state the previous call left. records (may be
+ * NULL) receives last_iter-first_iter+1 entries. */
+int sfseg_solve(sfseg_ctx* ctx, const sfseg_params* p, int32_t first_iter,
+                int32_t last_iter, sfseg_iter_record* records);
+
+/* Copies the current iterate (the projected unit vector after the last solved
+ * iteration) to soft (may be NULL) and threshold_final(soft, frac) to mask
+ * (may be NULL). */
+int sfseg_download(sfseg_ctx* ctx, double frac, float* soft, uint8_t* mask, int32_t mem);
+
+/* Per-iteration metrics of the current iterate against a reference vector
+ * (angle_degrees, metrics.cpp:22-38) and a ground-truth mask (jaccard of
+ * threshold_final(x, frac), metrics.cpp:58-69). Either input may be NULL. */
+int sfseg_metrics(sfseg_ctx* ctx, const float* reference, const uint8_t* ground_truth,
+                  double frac, double* angle_deg, double* iou, int32_t mem);
+
+/* One-shot sfseg::run: load + solve(1..iterations) + download. records may be
+ * NULL; otherwise it must hold p->iterations entries. */
+int sfseg_run(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+              int32_t channels, const float* unary, const float* const* pairwise,
+              const float* x0, const sfseg_params* p, float* soft, uint8_t* mask,
+              sfseg_iter_record* records, int32_t mem);
+
+/* ---- stateless operators (the other engine.o entry points) -------------- */
+
+/* sfseg_step (engine.cpp:141-166): sum over channels of the single-channel
+ * step, no normalisation. out has T*H*W floats. */
+int sfseg_step(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+               int32_t channels, const float* x, const float* unary,
+               const float* const* pairwise, const sfseg_params* p, float* out,
+               int32_t mem);
+
+/* sfseg_step_channel (engine.cpp:131-139). */
+int sfseg_step_channel(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                       const float* x, const float* unary, const float* pairwise,
+                       const sfseg_params* p, float* out, int32_t mem);
+
+/* normalize_l2 (engine.cpp:168-183). Uses the same deterministic per-frame
+ * fp64 reduction as sfseg_solve, so run() == normalize_l2(step()) bitwise. */
+int sfseg_normalize_l2(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                       const float* x, float* out, double* norm, int32_t mem);
+
+/* project_binary (engine.cpp:185-205). */
+int sfseg_project_binary(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                         const float* x, int32_t iter, const sfseg_params* p, float* out,
+                         int32_t mem);
+
+/* threshold_final (engine.cpp:207-214, volume.cpp:107-114). */
+int sfseg_threshold_final(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                          const float* x, double frac, uint8_t* mask, int32_t mem);
+
+/* convolve_separable (conv3d.cpp:171-185): x, then y, then t pass, zero
+ * padded, float accumulation in the reference's order (bit-exact). */
+int sfseg_convolve_separable(sfseg_ctx* ctx, uint32_t frames, uint32_t height,
+                             uint32_t width, const float* v, const int32_t radii[3],
+                             const double sigmas[3], float* out, int32_t mem);
+
+/* Number of logical separable convolutions performed by this library since
+ * load (separable_convolution_count, conv3d.cpp:64-66): 1 + 2C fields per
+ * channel-step are counted as 3 per channel, as the reference does. */
+uint64_t sfseg_separable_convolution_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFSEG_CUDA_H */

@@ -1,0 +1,349 @@
+// aux_kernels.cuh — the non-stencil device work of the SFSeg path:
+// validation, guard rescale, S^p, canonical reductions and their finalize,
+// the projection/materialise transform, hard mask, metrics, and the generic
+// (any-radius) multi-pass stencil used where no fused instantiation exists.
+#pragma once
+
+#include <math.h>
+
+#include "device_common.cuh"
+#include "sfseg_types.cuh"
+
+namespace sfk {
+
+constexpr int kAuxThreads = 256;
+
+struct Vol {  // pitched device volume view
+    float* p;
+    int T, H, W, pitch;
+    __host__ __device__ size_t at(int t, int y, int x) const {
+        return (static_cast<size_t>(t) * H + y) * pitch + x;
+    }
+};
+
+// grid-stride over (t, y, x) of a pitched volume, x fastest
+#define SFK_FOR_VOXELS(v, t, y, x)                                                      \
+    for (long long _i = blockIdx.x * (long long)blockDim.x + threadIdx.x,                \
+                   _n = (long long)(v).T * (v).H * (v).W;                                \
+         _i < _n; _i += (long long)gridDim.x * blockDim.x)                               \
+        for (int t = (int)(_i / ((long long)(v).H * (v).W)),                             \
+                 y = (int)((_i / (v).W) % (v).H), x = (int)(_i % (v).W), _once = 1;      \
+             _once; _once = 0)
+
+// FeatureVolume::validate (volume.cpp:72-84): finite, and >= 0 if required.
+__global__ void k_validate(Vol v, int need_nonneg, int* flags) {
+    int bad = 0;
+    SFK_FOR_VOXELS(v, t, y, x) {
+        const float a = v.p[v.at(t, y, x)];
+        if (!isfinite(a)) bad |= 1;
+        if (need_nonneg && a < 0.0f) bad |= 2;
+    }
+    if (bad) atomicOr(flags, bad);
+}
+
+// per-block min/max for the unit-range guard (engine.cpp:229-233)
+__global__ void k_minmax_blocks(Vol v, float* bmin, float* bmax) {
+    __shared__ float smin[kAuxThreads], smax[kAuxThreads];
+    float lo = INFINITY, hi = -INFINITY;
+    SFK_FOR_VOXELS(v, t, y, x) {
+        const float a = v.p[v.at(t, y, x)];
+        lo = fminf(lo, a);
+        hi = fmaxf(hi, a);
+    }
+    smin[threadIdx.x] = lo;
+    smax[threadIdx.x] = hi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            smin[threadIdx.x] = fminf(smin[threadIdx.x], smin[threadIdx.x + s]);
+            smax[threadIdx.x] = fmaxf(smax[threadIdx.x], smax[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        bmin[blockIdx.x] = smin[0];
+        bmax[blockIdx.x] = smax[0];
+    }
+}
+
+__global__ void k_minmax_final(const float* bmin, const float* bmax, int n, float* out2) {
+    __shared__ float smin[kAuxThreads], smax[kAuxThreads];
+    float lo = INFINITY, hi = -INFINITY;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        lo = fminf(lo, bmin[i]);
+        hi = fmaxf(hi, bmax[i]);
+    }
+    smin[threadIdx.x] = lo;
+    smax[threadIdx.x] = hi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            smin[threadIdx.x] = fminf(smin[threadIdx.x], smin[threadIdx.x + s]);
+            smax[threadIdx.x] = fmaxf(smax[threadIdx.x], smax[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out2[0] = smin[0];
+        out2[1] = smax[0];
+    }
+}
+
+// scale_channel_into_unit_range (engine.cpp:234-242): IEEE ops, no FMA.
+__global__ void k_unit_range(Vol v, const float* lohi) {
+    const float lo = lohi[0], hi = lohi[1];
+    if (lo >= 0.0f && hi <= 1.0f) return;  // leave the bits alone
+    SFK_FOR_VOXELS(v, t, y, x) {
+        float& a = v.p[v.at(t, y, x)];
+        if (hi > lo)
+            a = __fdiv_rn(__fsub_rn(a, lo), __fsub_rn(hi, lo));
+        else
+            a = fminf(fmaxf(lo, 0.0f), 1.0f);
+    }
+}
+
+// pow_volume (engine.cpp:52-71): float(pow(double s, p)); p==0 -> 1, p==1 -> copy
+__global__ void k_pow(Vol s, Vol out, double p) {
+    SFK_FOR_VOXELS(s, t, y, x) {
+        const float a = s.p[s.at(t, y, x)];
+        float r;
+        if (p == 0.0)
+            r = 1.0f;
+        else if (p == 1.0)
+            r = a;
+        else
+            r = static_cast<float>(pow(static_cast<double>(a), p));
+        out.p[out.at(t, y, x)] = r;
+    }
+}
+
+// Canonical sum(x^2) partials + per-frame max over an existing volume.
+// One warp per (frame, 4-row band, 32-column half); lanes = columns.
+__global__ void k_partials(Vol v, double* part, float* frame_max, int nbands, int nhalves,
+                           int t_off) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = (long long)v.T * nbands * nhalves;
+    if (warp >= nwarps) return;
+    const int half = warp % nhalves;
+    const int band = (warp / nhalves) % nbands;
+    const int t = warp / (nhalves * nbands);
+    const int x = half * 32 + lane;
+    double colsum = 0.0;
+    float m = 0.0f;
+    for (int r = 0; r < 4; ++r) {
+        const int y = band * 4 + r;
+        float a = 0.0f;
+        if (x < v.W && y < v.H) a = v.p[v.at(t, y, x)];
+        colsum += static_cast<double>(a) * static_cast<double>(a);
+        m = fmaxf(m, a);
+    }
+    const double s = butterfly_sum32(colsum);
+    m = butterfly_max32(m);
+    if (lane == 0) {
+        part[(static_cast<size_t>(t + t_off) * nbands + band) * nhalves + half] = s;
+        atomic_max_nonneg(frame_max + t + t_off, m);
+    }
+}
+
+// frame_sum[t] = fixed-order reduction of the frame's partials: thread i sums
+// entries i, i+256, ... sequentially; then a fixed shared-memory tree.
+__global__ void k_finalize_frames(const double* part, int per_frame, double* frame_sum,
+                                  int t0) {
+    __shared__ double s[kAuxThreads];
+    const int t = blockIdx.x + t0;
+    const double* p = part + static_cast<size_t>(t) * per_frame;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < per_frame; i += blockDim.x) acc += p[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) frame_sum[t] = s[0];
+}
+
+// Total over frames (fixed order: same tree as above over frame index) and
+// the scalars the next iteration applies on load (engine.cpp:168-205).
+// mode_next: 1 = normalise, 2 = normalise + sigmoid; lambda from the host.
+__global__ void k_finalize_total(const double* frame_sum, float* frame_max, int T,
+                                 IterState* st, double* norms, int iter_index, int mode_next,
+                                 double lambda, double threshold_frac) {
+    __shared__ double s[kAuxThreads];
+    __shared__ float sm[kAuxThreads];
+    double acc = 0.0;
+    float m = 0.0f;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+        acc += frame_sum[i];
+        m = fmaxf(m, frame_max[i]);
+        frame_max[i] = 0.0f;  // reset for the next iteration
+    }
+    s[threadIdx.x] = acc;
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) {
+            s[threadIdx.x] += s[threadIdx.x + k];
+            sm[threadIdx.x] = fmaxf(sm[threadIdx.x], sm[threadIdx.x + k]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double norm = sqrt(s[0]);
+        if (norms) norms[iter_index] = norm;
+        IterState n = *st;
+        n.norm = norm;
+        if (norm == 0.0) {
+            n.degenerate = 1;
+        } else if (!n.degenerate) {
+            n.inv = 1.0 / norm;
+            n.max_raw = sm[0];
+            // max of the unit vector: the map y -> float(double(y)*inv) is monotone
+            n.max_unit = static_cast<float>(static_cast<double>(sm[0]) * n.inv);
+            n.mode = mode_next;
+            n.lambda = lambda;
+            n.theta = threshold_frac * static_cast<double>(n.max_unit);
+        }
+        *st = n;
+    }
+}
+
+// x = T(y): the projection of the state, materialised into a volume.
+__global__ void k_transform(Vol y, Vol out, const IterState* stp) {
+    const IterState st = *stp;
+    SFK_FOR_VOXELS(y, t, yy, x) {
+        const float a = y.p[y.at(t, yy, x)];
+        float r = a;
+        if (st.mode >= 1) r = static_cast<float>(static_cast<double>(a) * st.inv);
+        if (st.mode == 2) {
+            const double z = st.lambda * (static_cast<double>(r) - st.theta);
+            r = static_cast<float>(1.0 / (1.0 + exp(-z)));
+        }
+        out.p[out.at(t, yy, x)] = r;
+    }
+}
+
+// max(0, max v) (engine.cpp:189-190, 208-210)
+__global__ void k_max(Vol v, float* out) {
+    float m = 0.0f;
+    SFK_FOR_VOXELS(v, t, y, x) m = fmaxf(m, v.p[v.at(t, y, x)]);
+    m = butterfly_max32(m);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
+}
+
+// mask_from_volume with cut = float(frac * max) (engine.cpp:212, volume.cpp:107-114)
+__global__ void k_mask(Vol v, const float* maxp, double frac, uint8_t* mask) {
+    const float cut = static_cast<float>(frac * static_cast<double>(*maxp));
+    SFK_FOR_VOXELS(v, t, y, x) {
+        mask[(static_cast<size_t>(t) * v.H + y) * v.W + x] = v.p[v.at(t, y, x)] > cut ? 1 : 0;
+    }
+}
+
+// angle_degrees / jaccard accumulators (metrics.cpp:22-38, 58-69)
+__global__ void k_metrics(Vol xv, Vol ref, const uint8_t* gt, const float* maxp, double frac,
+                          double* acc3, unsigned long long* cnt2) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    unsigned long long inter = 0, uni = 0;
+    const float cut = maxp ? static_cast<float>(frac * static_cast<double>(*maxp)) : 0.0f;
+    SFK_FOR_VOXELS(xv, t, y, x) {
+        const double a = xv.p[xv.at(t, y, x)];
+        if (ref.p) {
+            const double b = ref.p[ref.at(t, y, x)];
+            dot += a * b;
+            na += a * a;
+            nb += b * b;
+        }
+        if (gt) {
+            const bool va = xv.p[xv.at(t, y, x)] > cut;
+            const bool vb = gt[(static_cast<size_t>(t) * xv.H + y) * xv.W + x] != 0;
+            inter += (va && vb);
+            uni += (va || vb);
+        }
+    }
+    if (ref.p) {
+        atomicAdd(acc3 + 0, dot);
+        atomicAdd(acc3 + 1, na);
+        atomicAdd(acc3 + 2, nb);
+    }
+    if (gt) {
+        atomicAdd(cnt2 + 0, inter);
+        atomicAdd(cnt2 + 1, uni);
+    }
+}
+
+// ---- generic (any-radius) stencil: conv3d.cpp:80-167 on pitched volumes --
+
+struct Taps {
+    float t[64], y[64], x[64];
+    int rt, ry, rx;
+};
+
+// products u, fu, f2u (engine.cpp:92-100) with the load transform
+__global__ void k_products(Vol xsrc, Vol sp, Vol f, Vol u, Vol fu, Vol f2u,
+                           const IterState* stp) {
+    const IterState st = *stp;
+    SFK_FOR_VOXELS(xsrc, t, y, x) {
+        const float yv = xsrc.p[xsrc.at(t, y, x)];
+        float xv = yv;
+        if (st.mode >= 1) xv = static_cast<float>(static_cast<double>(yv) * st.inv);
+        if (st.mode == 2) {
+            const double z = st.lambda * (static_cast<double>(xv) - st.theta);
+            xv = static_cast<float>(1.0 / (1.0 + exp(-z)));
+        }
+        const float uu = xmul(sp.p[sp.at(t, y, x)], xv);
+        const float fv = f.p[f.at(t, y, x)];
+        u.p[u.at(t, y, x)] = uu;
+        fu.p[fu.at(t, y, x)] = xmul(fv, uu);
+        f2u.p[f2u.at(t, y, x)] = xmul(xmul(fv, fv), uu);
+    }
+}
+
+__global__ void k_pass_x(Vol in, Vol out, const __grid_constant__ Taps k) {
+    SFK_FOR_VOXELS(in, t, y, x) {
+        float acc = 0.0f;
+        const int dlo = -min(k.rx, x), dhi = min(k.rx, in.W - 1 - x);
+        for (int d = dlo; d <= dhi; ++d) acc = xadd(acc, xmul(k.x[d + k.rx], in.p[in.at(t, y, x + d)]));
+        out.p[out.at(t, y, x)] = acc;
+    }
+}
+
+__global__ void k_pass_y(Vol in, Vol out, const __grid_constant__ Taps k) {
+    SFK_FOR_VOXELS(in, t, y, x) {
+        const int dlo = -min(k.ry, y), dhi = min(k.ry, in.H - 1 - y);
+        float acc = 0.0f;
+        for (int d = dlo; d <= dhi; ++d) {
+            const float p = xmul(k.y[d + k.ry], in.p[in.at(t, y + d, x)]);
+            acc = (d == dlo) ? p : xadd(acc, p);
+        }
+        out.p[out.at(t, y, x)] = acc;
+    }
+}
+
+__global__ void k_pass_t(Vol in, Vol out, const __grid_constant__ Taps k) {
+    SFK_FOR_VOXELS(in, t, y, x) {
+        const int dlo = -min(k.rt, t), dhi = min(k.rt, in.T - 1 - t);
+        float acc = 0.0f;
+        for (int d = dlo; d <= dhi; ++d) {
+            const float p = xmul(k.t[d + k.rt], in.p[in.at(t + d, y, x)]);
+            acc = (d == dlo) ? p : xadd(acc, p);
+        }
+        out.p[out.at(t, y, x)] = acc;
+    }
+}
+
+// recombination + channel accumulation (engine.cpp:113-119, 157-162)
+__global__ void k_recombine(Vol a, Vol b, Vol c, Vol sp, Vol f, Vol out, float inv_alpha,
+                            int first) {
+    SFK_FOR_VOXELS(a, t, y, x) {
+        const float fv = f.p[f.at(t, y, x)];
+        const float t1 = xmul(xsub(inv_alpha, xmul(fv, fv)), a.p[a.at(t, y, x)]);
+        const float t2 = xsub(t1, b.p[b.at(t, y, x)]);
+        const float t3 = xadd(t2, xmul(xmul(2.0f, fv), c.p[c.at(t, y, x)]));
+        const float term = xmul(sp.p[sp.at(t, y, x)], t3);
+        float& o = out.p[out.at(t, y, x)];
+        o = first ? term : xadd(o, term);
+    }
+}
+
+}  // namespace sfk

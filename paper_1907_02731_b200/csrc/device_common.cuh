@@ -1,0 +1,102 @@
+// device_common.cuh — sm_100a primitives shared by the SFSeg kernels:
+// TMA tensor loads with mbarrier completion, exact (non-contracted) fp32
+// arithmetic matching the reference's SSE2 build, and the canonical
+// deterministic reduction of sum(x^2) used by every kernel that feeds the
+// L2 norm (normalize_l2, engine.cpp:168-183).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfk {
+
+// ---------------------------------------------------------------------------
+// Exact fp32 helpers. The reference is compiled for baseline x86-64 (SSE2, no
+// FMA), so every product and sum is rounded on its own. __fmul_rn/__fadd_rn
+// are never contracted by nvcc/ptxas.
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b); }
+
+// ---------------------------------------------------------------------------
+// mbarrier + TMA (cp.async.bulk.tensor) wrappers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 3-D tiled tensor load, box {BW, BH, 1} at (x, y, t); out-of-bounds elements
+// (negative or past the tensor extent) are filled with +0.0f by the TMA unit,
+// which is exactly the reference's zero padding (conv3d.cpp:93-95).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int t) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(t), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Canonical sum-of-squares reduction (deterministic, independent of tiling,
+// launch geometry and GPU count):
+//   block  = 8 consecutive rows (y0 % 8 == 0) x 32 consecutive columns
+//            (x0 % 32 == 0) of one frame;
+//   column = sequential fp64 sum of x^2 over the 8 rows, top to bottom;
+//   block  = xor-butterfly (16, 8, 4, 2, 1) over the 32 column sums;
+//   frame  = finalize_frames kernel (fixed order over blocks);
+//   total  = finalize_total kernel (fixed order over frames).
+// Entries outside the volume count as 0.
+__device__ __forceinline__ double butterfly_sum32(double v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float butterfly_max32(float v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// max over nonnegative floats (seeded at 0, engine.cpp:189-190) via int
+// ordering of the IEEE bit patterns.
+__device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
+    if (v > 0.0f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+}
+
+}  // namespace sfk

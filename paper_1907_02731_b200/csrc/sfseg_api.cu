@@ -1,0 +1,1076 @@
+// sfseg_api.cu — host driver of the B200 SFSeg library and implementation of
+// the C ABI declared in include/sfseg_cuda.h.
+//
+// Per iteration of Algorithm 1 (engine.cpp:284-341) the context launches, on
+// its own stream: the fused stencil kernel once per channel group
+// (fused_step.cuh), k_finalize_frames and k_finalize_total. No host
+// synchronisation happens inside the loop; norms and the projection scalars
+// stay on the device (IterState) until the solve ends.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sfseg_cuda.h"
+#include "aux_kernels.cuh"
+#include "fused_step.cuh"
+
+namespace {
+
+using sfk::FusedArgs;
+using sfk::IterState;
+using sfk::Vol;
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_conv_count{0};
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what);
+
+// After every launch: launch errors always; with SFSEG_DEBUG_SYNC=1 also a
+// stream sync so an asynchronous fault is attributed to the right kernel.
+void launched(cudaStream_t s, const char* what) {
+    static const bool dbg = [] {
+        const char* v = std::getenv("SFSEG_DEBUG_SYNC");
+        return v && *v && *v != '0';
+    }();
+    ck(cudaGetLastError(), what);
+    if (dbg) ck(cudaStreamSynchronize(s), what);
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation)
+        fail(SFSEG_ERR_CAPACITY, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(SFSEG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        g_err.clear();
+        return SFSEG_OK;
+    } catch (const Fail& f) {
+        g_err = f.msg;
+        return f.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SFSEG_ERR_STATE;
+    }
+}
+
+// ---- taps: make_gaussian_kernel (conv3d.cpp:23-58), fp64 on the host ------
+std::vector<double> raw_taps(double sigma, int r) {
+    std::vector<double> t(2 * r + 1);
+    const double inv = 1.0 / (2.0 * sigma * sigma);
+    for (int i = -r; i <= r; ++i) t[i + r] = std::exp(-static_cast<double>(i) * i * inv);
+    return t;
+}
+
+struct HostKernel {
+    std::vector<double> t, y, x;
+    int rt, ry, rx;
+};
+
+HostKernel make_kernel(const int32_t radii[3], const double sigmas[3]) {
+    for (int a = 0; a < 3; ++a)
+        if (!(sigmas[a] > 0.0)) fail(SFSEG_ERR_PARAMETER, "kernel sigma must be positive");
+    for (int a = 0; a < 3; ++a)
+        if (radii[a] < 0) fail(SFSEG_ERR_PARAMETER, "kernel radius must be nonnegative");
+    HostKernel k;
+    k.rt = radii[0];
+    k.ry = radii[1];
+    k.rx = radii[2];
+    k.t = raw_taps(sigmas[0], radii[0]);
+    k.y = raw_taps(sigmas[1], radii[1]);
+    k.x = raw_taps(sigmas[2], radii[2]);
+    auto sum = [](const std::vector<double>& v) {
+        double s = 0.0;
+        for (double a : v) s += a;
+        return s;
+    };
+    const double total = sum(k.t) * sum(k.y) * sum(k.x);
+    for (double& a : k.t) a /= total;
+    return k;
+}
+
+void validate_params(const sfseg_params* c) {
+    if (!c) fail(SFSEG_ERR_PARAMETER, "null params");
+    // engine.cpp:21-42, same order and messages
+    if (!(c->alpha > 0.0)) fail(SFSEG_ERR_PARAMETER, "alpha must be positive");
+    if (c->p < 0.0) fail(SFSEG_ERR_PARAMETER, "p must be nonnegative");
+    if (c->iterations < 1) fail(SFSEG_ERR_PARAMETER, "iterations must be at least 1");
+    if (c->binarize_start < 1) fail(SFSEG_ERR_PARAMETER, "binarize_start must be at least 1");
+    if (!(c->sigmoid_slope0 > 0.0)) fail(SFSEG_ERR_PARAMETER, "sigmoid_slope0 must be positive");
+    if (!(c->slope_growth >= 1.0)) fail(SFSEG_ERR_PARAMETER, "slope_growth must be >= 1");
+    if (!(c->threshold_frac > 0.0 && c->threshold_frac < 1.0))
+        fail(SFSEG_ERR_PARAMETER, "threshold_frac must lie in (0,1)");
+    if (!(c->final_threshold > 0.0 && c->final_threshold < 1.0))
+        fail(SFSEG_ERR_PARAMETER, "final_threshold must lie in (0,1)");
+    for (int a = 0; a < 3; ++a)
+        if (!(c->sigmas[a] > 0.0)) fail(SFSEG_ERR_PARAMETER, "kernel sigma must be positive");
+    for (int a = 0; a < 3; ++a)
+        if (c->radii[a] < 0) fail(SFSEG_ERR_PARAMETER, "kernel radius must be nonnegative");
+    if (c->temporal_window >= 0 && c->temporal_window < c->radii[0])
+        fail(SFSEG_ERR_PARAMETER, "temporal_window must cover the kernel time radius");
+    if (!c->allow_negative_affinity && c->alpha > 1.0)
+        fail(SFSEG_ERR_PARAMETER,
+             "alpha > 1 can produce negative affinities; enable allow_negative_affinity or "
+             "reduce alpha");
+    if (c->arith != SFSEG_ARITH_EXACT && c->arith != SFSEG_ARITH_FAST)
+        fail(SFSEG_ERR_PARAMETER, "arith must be SFSEG_ARITH_EXACT or SFSEG_ARITH_FAST");
+}
+
+// ---- TMA descriptor encoding via the driver entry point -------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) fail(SFSEG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_tmap(const float* base, int frames, int H, int W, int pitch, int box_w,
+                      int box_h) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(frames)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch) * 4,
+                                   static_cast<cuuint64_t>(pitch) * H * 4};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                   const_cast<float*>(base), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SFSEG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+// ---- fused kernel registry -------------------------------------------------
+// Each instantiation covers radii up to (RT, R) by zero-padding the taps:
+// zero taps add +0 to the float sums, which leaves every value unchanged.
+struct FusedVariant {
+    int rt, r, ty;
+    size_t smem;
+    int threads;
+    void (*kernel)(FusedArgs);
+    int box_w, box_h;
+};
+
+template <int RT, int R, int TY, int QY>
+FusedVariant variant() {
+    using G = sfk::FusedGeom<RT, R, 1, TY, 64, QY, 2>;
+    FusedVariant v;
+    v.rt = RT;
+    v.r = R;
+    v.ty = TY;
+    v.smem = G::SMEM_BYTES;
+    v.threads = G::NT;
+    v.kernel = sfk::fused_step_exact<RT, R, 1, TY, QY, 2>;
+    v.box_w = G::BW;
+    v.box_h = G::BH;
+    return v;
+}
+
+const std::vector<FusedVariant>& variants() {
+    static const std::vector<FusedVariant> v = {
+        variant<1, 2, 32, 8>(), variant<1, 3, 32, 8>(), variant<2, 4, 32, 8>(),
+        variant<2, 5, 32, 8>(),
+    };
+    return v;
+}
+
+bool env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v && *v != '0';
+}
+
+const FusedVariant* pick_variant(int rt, int ry, int rx) {
+    static const bool force_generic = env_flag("SFSEG_FORCE_GENERIC");
+    if (force_generic) return nullptr;
+    const int r = std::max(ry, rx);
+    const FusedVariant* best = nullptr;
+    for (const auto& v : variants())
+        if (v.rt >= rt && v.r >= r) {
+            const long cost = (2L * v.rt + 1) * (2L * v.r + 1);
+            if (!best || cost < (2L * best->rt + 1) * (2L * best->r + 1)) best = &v;
+        }
+    return best;
+}
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct sfseg_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    // resident problem
+    int T = 0, H = 0, W = 0, P = 0, C = 0;
+    bool loaded = false;    // buffers allocated for (T, H, W, C)
+    bool resident = false;  // a problem from sfseg_load is in S/F/x0
+    bool has_x0 = false;
+    float* S = nullptr;
+    float* sp = nullptr;
+    std::vector<float*> F;       // raw channels as uploaded
+    std::vector<float*> Fw;      // guard-rescaled working copies (may alias F)
+    bool guard_applied = false;  // Fw reflects the allow_negative_affinity=false guard
+    float* x0 = nullptr;
+    float* y[2] = {nullptr, nullptr};
+    int cur = -1;                // index into y of the current raw iterate (-1: none)
+    double sp_p = NAN;           // p that sp was computed for
+    // scratch
+    double* part = nullptr;
+    size_t part_elems = 0;
+    double* frame_sum = nullptr;
+    float* frame_max = nullptr;
+    IterState* st = nullptr;     // solve state
+    IterState* st_aux = nullptr; // stateless operators
+    double* norms = nullptr;
+    int norms_cap = 0;
+    int* flags = nullptr;
+    float* scratch_f = nullptr;  // 2 floats + block min/max
+    float* bminmax = nullptr;
+    double* acc3 = nullptr;
+    unsigned long long* cnt2 = nullptr;
+    // generic-path temporaries (allocated lazily)
+    std::vector<float*> tmp;
+    // timing
+    bool timing = false;
+    sfseg_timing last_timing{};
+    std::vector<cudaEvent_t> ev;
+    std::mutex mu;
+
+    size_t vol_elems() const { return static_cast<size_t>(T) * H * P; }
+    Vol vol(float* p) const { return Vol{p, T, H, W, P}; }
+    int nbands() const { return (H + 3) / 4; }
+    int nhalves() const { return (W + 31) / 32; }
+};
+
+namespace {
+
+void dfree(float*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+float* dalloc_vol(sfseg_ctx* c) {
+    float* p = nullptr;
+    ck(cudaMalloc(&p, c->vol_elems() * sizeof(float)), "cudaMalloc volume");
+    // zero the pitch padding once; kernels never read past W, TMA treats it as OOB
+    ck(cudaMemsetAsync(p, 0, c->vol_elems() * sizeof(float), c->stream), "memset");
+    return p;
+}
+
+void release_problem(sfseg_ctx* c) {
+    if (c->guard_applied)
+        for (size_t i = 0; i < c->Fw.size(); ++i)
+            if (c->Fw[i] != c->F[i]) dfree(c->Fw[i]);
+    c->Fw.clear();
+    for (auto*& f : c->F) dfree(f);
+    c->F.clear();
+    dfree(c->S);
+    dfree(c->sp);
+    dfree(c->x0);
+    dfree(c->y[0]);
+    dfree(c->y[1]);
+    for (auto*& t : c->tmp) dfree(t);
+    c->tmp.clear();
+    if (c->part) cudaFree(c->part);
+    if (c->frame_sum) cudaFree(c->frame_sum);
+    if (c->frame_max) cudaFree(c->frame_max);
+    c->part = nullptr;
+    c->frame_sum = nullptr;
+    c->frame_max = nullptr;
+    c->loaded = false;
+    c->resident = false;
+    c->cur = -1;
+    c->sp_p = NAN;
+    c->guard_applied = false;
+}
+
+void check_shape(uint32_t T, uint32_t H, uint32_t W) {
+    if (T == 0 || H == 0 || W == 0) fail(SFSEG_ERR_VALIDATION, "volume shape has an empty axis");
+    if (T > (1u << 30) || H > (1u << 20) || W > (1u << 20))
+        fail(SFSEG_ERR_CAPACITY, "volume shape exceeds the supported extent");
+}
+
+void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
+    if (c->loaded && c->T == (int)T && c->H == (int)H && c->W == (int)W && c->C == C) return;
+    release_problem(c);
+    c->T = T;
+    c->H = H;
+    c->W = W;
+    c->P = round_up(static_cast<int>(W), 32);
+    c->C = C;
+    c->S = dalloc_vol(c);
+    c->sp = dalloc_vol(c);
+    for (int i = 0; i < C; ++i) c->F.push_back(dalloc_vol(c));
+    c->Fw = c->F;
+    c->y[0] = dalloc_vol(c);
+    c->y[1] = dalloc_vol(c);
+    c->part_elems = static_cast<size_t>(T) * c->nbands() * c->nhalves();
+    ck(cudaMalloc(&c->part, c->part_elems * sizeof(double)), "cudaMalloc partials");
+    ck(cudaMalloc(&c->frame_sum, T * sizeof(double)), "cudaMalloc frame sums");
+    ck(cudaMalloc(&c->frame_max, T * sizeof(float)), "cudaMalloc frame max");
+    ck(cudaMemsetAsync(c->frame_max, 0, T * sizeof(float), c->stream), "memset");
+    c->loaded = true;
+}
+
+// dense (T,H,W) host/device -> pitched device
+void upload(sfseg_ctx* c, float* dst, const float* src, int32_t mem) {
+    const cudaMemcpyKind kind = mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyHostToDevice;
+    ck(cudaMemcpy2DAsync(dst, c->P * sizeof(float), src, c->W * sizeof(float),
+                         c->W * sizeof(float), static_cast<size_t>(c->T) * c->H, kind,
+                         c->stream),
+       "upload volume");
+}
+
+void download(sfseg_ctx* c, float* dst, const float* src, int32_t mem) {
+    const cudaMemcpyKind kind = mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyDeviceToHost;
+    ck(cudaMemcpy2DAsync(dst, c->W * sizeof(float), src, c->P * sizeof(float),
+                         c->W * sizeof(float), static_cast<size_t>(c->T) * c->H, kind,
+                         c->stream),
+       "download volume");
+}
+
+int aux_grid(sfseg_ctx* c) { return c->num_sms * 8; }
+
+void validate_vol(sfseg_ctx* c, float* v, bool nonneg, const char* what) {
+    ck(cudaMemsetAsync(c->flags, 0, sizeof(int), c->stream), "memset flags");
+    sfk::k_validate<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(v), nonneg, c->flags);
+    launched(c->stream, "k_validate");
+    int h = 0;
+    ck(cudaMemcpyAsync(&h, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flags");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (h & 1) fail(SFSEG_ERR_VALIDATION, std::string(what) + " contains a non-finite value");
+    if (h & 2)
+        fail(SFSEG_ERR_VALIDATION,
+             std::string(what) + ": unary/solution volume contains a negative value");
+}
+
+// S^p for the resident S (cached per p)
+void ensure_sp(sfseg_ctx* c, double p) {
+    if (c->sp_p == p) return;
+    sfk::k_pow<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->S), c->vol(c->sp), p);
+    launched(c->stream, "k_pow");
+    c->sp_p = p;
+}
+
+// guard rescale of the pairwise channels (engine.cpp:255-259)
+void ensure_guard(sfseg_ctx* c, bool guard) {
+    if (!guard) {
+        if (c->guard_applied) {
+            for (size_t i = 0; i < c->Fw.size(); ++i)
+                if (c->Fw[i] != c->F[i]) dfree(c->Fw[i]);
+            c->Fw = c->F;
+            c->guard_applied = false;
+        }
+        return;
+    }
+    if (c->guard_applied) return;
+    const int nb = aux_grid(c);
+    for (int i = 0; i < c->C; ++i) {
+        sfk::k_minmax_blocks<<<nb, sfk::kAuxThreads, 0, c->stream>>>(
+            c->vol(c->F[i]), c->bminmax, c->bminmax + nb);
+        sfk::k_minmax_final<<<1, sfk::kAuxThreads, 0, c->stream>>>(c->bminmax, c->bminmax + nb,
+                                                                 nb, c->scratch_f);
+        float lohi[2];
+        ck(cudaMemcpyAsync(lohi, c->scratch_f, sizeof lohi, cudaMemcpyDeviceToHost, c->stream),
+           "minmax");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        if (lohi[0] >= 0.0f && lohi[1] <= 1.0f) continue;  // bits untouched
+        float* w = dalloc_vol(c);
+        ck(cudaMemcpyAsync(w, c->F[i], c->vol_elems() * sizeof(float), cudaMemcpyDeviceToDevice,
+                           c->stream),
+           "copy channel");
+        sfk::k_unit_range<<<nb, sfk::kAuxThreads, 0, c->stream>>>(c->vol(w), c->scratch_f);
+        launched(c->stream, "k_unit_range");
+        c->Fw[i] = w;
+    }
+    c->guard_applied = true;
+}
+
+void fill_taps(FusedArgs& a, const HostKernel& k, const FusedVariant& v) {
+    std::memset(a.taps_x, 0, sizeof a.taps_x);
+    std::memset(a.taps_y, 0, sizeof a.taps_y);
+    std::memset(a.taps_t, 0, sizeof a.taps_t);
+    // centre the real taps inside the variant's support; outer taps stay 0
+    for (int i = 0; i <= 2 * k.rx; ++i) a.taps_x[v.r - k.rx + i] = static_cast<float>(k.x[i]);
+    for (int i = 0; i <= 2 * k.ry; ++i) a.taps_y[v.r - k.ry + i] = static_cast<float>(k.y[i]);
+    for (int i = 0; i <= 2 * k.rt; ++i) a.taps_t[v.rt - k.rt + i] = static_cast<float>(k.t[i]);
+}
+
+float* tmp_vol(sfseg_ctx* c, size_t i) {
+    while (c->tmp.size() <= i) c->tmp.push_back(dalloc_vol(c));
+    return c->tmp[i];
+}
+
+// One step y_out = sum_c step_c(T(x_src)) with fused kernels or the generic
+// multi-pass path; emits canonical partials + frame max into c->part /
+// c->frame_max for the whole volume.
+void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
+                 const IterState* st, float* out, const std::vector<float*>& Fch) {
+    const float inv_alpha = static_cast<float>(1.0 / alpha);
+    const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx);
+    g_conv_count.fetch_add(3ull * Fch.size(), std::memory_order_relaxed);
+    if (v) {
+        FusedArgs a;
+        std::memset(&a, 0, sizeof a);
+        a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+        a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+        a.sp = c->sp;
+        a.out = out;
+        a.part = c->part;
+        a.frame_max = c->frame_max;
+        a.st = st;
+        fill_taps(a, k, *v);
+        a.inv_alpha = inv_alpha;
+        a.T = c->T;
+        a.H = c->H;
+        a.W = c->W;
+        a.pitch = c->P;
+        a.buf_t0 = 0;
+        a.out_t0 = 0;
+        a.out_t1 = c->T;
+        a.out_buf_t0 = 0;
+        a.tiles_x = (c->W + 63) / 64;
+        a.tiles_y = (c->H + v->ty - 1) / v->ty;
+        a.nbands = c->nbands();
+        a.nhalves = c->nhalves();
+        const long long units = static_cast<long long>(a.tiles_x) * a.tiles_y * c->T;
+        const long long grid = std::min<long long>(c->num_sms, units);
+        a.units_per_cta = (units + grid - 1) / grid;
+        static bool attr_set[64] = {};
+        const int vidx = static_cast<int>(v - variants().data());
+        if (!attr_set[vidx]) {
+            ck(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(v->smem)),
+               "cudaFuncSetAttribute");
+            attr_set[vidx] = true;
+        }
+        const int grid_n = static_cast<int>((units + a.units_per_cta - 1) / a.units_per_cta);
+        for (size_t g = 0; g < Fch.size(); ++g) {
+            a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+            a.f[0] = Fch[g];
+            a.first_group = g == 0;
+            a.last_group = g + 1 == Fch.size();
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (c->timing) {
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0, c->stream);
+            }
+            v->kernel<<<grid_n, v->threads, v->smem, c->stream>>>(a);
+            launched(c->stream, "fused_step launch");
+            if (c->timing) {
+                cudaEventRecord(e1, c->stream);
+                c->ev.push_back(e0);
+                c->ev.push_back(e1);
+            }
+        }
+        return;
+    }
+    // generic multi-pass path (radii beyond the fused instantiations)
+    sfk::Taps tp;
+    std::memset(&tp, 0, sizeof tp);
+    if (k.rt > 31 || k.ry > 31 || k.rx > 31) fail(SFSEG_ERR_CAPACITY, "kernel radius above 31");
+    for (int i = 0; i <= 2 * k.rt; ++i) tp.t[i] = static_cast<float>(k.t[i]);
+    for (int i = 0; i <= 2 * k.ry; ++i) tp.y[i] = static_cast<float>(k.y[i]);
+    for (int i = 0; i <= 2 * k.rx; ++i) tp.x[i] = static_cast<float>(k.x[i]);
+    tp.rt = k.rt;
+    tp.ry = k.ry;
+    tp.rx = k.rx;
+    const int g = aux_grid(c), bt = sfk::kAuxThreads;
+    float *u = tmp_vol(c, 0), *fu = tmp_vol(c, 1), *f2u = tmp_vol(c, 2);
+    float *ca = tmp_vol(c, 3), *cb = tmp_vol(c, 4), *cc = tmp_vol(c, 5);
+    float *t0 = tmp_vol(c, 6), *t1 = tmp_vol(c, 7);
+    Vol xs = c->vol(const_cast<float*>(x_src));
+    for (size_t ch = 0; ch < Fch.size(); ++ch) {
+        sfk::k_products<<<g, bt, 0, c->stream>>>(xs, c->vol(c->sp), c->vol(Fch[ch]), c->vol(u),
+                                                 c->vol(fu), c->vol(f2u), st);
+        const float* srcs[3] = {u, f2u, fu};
+        float* dsts[3] = {ca, cb, cc};
+        for (int q = 0; q < 3; ++q) {
+            sfk::k_pass_x<<<g, bt, 0, c->stream>>>(c->vol(const_cast<float*>(srcs[q])), c->vol(t0), tp);
+            sfk::k_pass_y<<<g, bt, 0, c->stream>>>(c->vol(t0), c->vol(t1), tp);
+            sfk::k_pass_t<<<g, bt, 0, c->stream>>>(c->vol(t1), c->vol(dsts[q]), tp);
+        }
+        sfk::k_recombine<<<g, bt, 0, c->stream>>>(c->vol(ca), c->vol(cb), c->vol(cc),
+                                                  c->vol(c->sp), c->vol(Fch[ch]), c->vol(out),
+                                                  inv_alpha, ch == 0);
+        launched(c->stream, "generic step");
+    }
+    const long long warps = static_cast<long long>(c->T) * c->nbands() * c->nhalves();
+    sfk::k_partials<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, c->stream>>>(
+        c->vol(out), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
+    launched(c->stream, "k_partials");
+}
+
+void finalize(sfseg_ctx* c, IterState* st, double* norms, int iter_index, int mode_next,
+              double lambda, double frac) {
+    const int per_frame = c->nbands() * c->nhalves();
+    sfk::k_finalize_frames<<<c->T, sfk::kAuxThreads, 0, c->stream>>>(c->part, per_frame,
+                                                                   c->frame_sum, 0);
+    sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
+        c->frame_sum, c->frame_max, c->T, st, norms, iter_index, mode_next, lambda, frac);
+    launched(c->stream, "finalize");
+}
+
+void set_state(sfseg_ctx* c, IterState* dst, const IterState& s) {
+    ck(cudaMemcpyAsync(dst, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state");
+}
+
+IterState get_state(sfseg_ctx* c, const IterState* src) {
+    IterState s;
+    ck(cudaMemcpyAsync(&s, src, sizeof s, cudaMemcpyDeviceToHost, c->stream), "state");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return s;
+}
+
+double lambda_for(const sfseg_params* p, int iter) {
+    return p->sigmoid_slope0 * std::pow(p->slope_growth, iter - p->binarize_start);
+}
+
+// iterate currently visible to the caller = T_state(y[cur]) (or S/x0 before
+// the first iteration)
+void materialize(sfseg_ctx* c, float* out) {
+    if (c->cur < 0) {
+        ck(cudaMemcpyAsync(out, c->has_x0 ? c->x0 : c->S, c->vol_elems() * sizeof(float),
+                           cudaMemcpyDeviceToDevice, c->stream),
+           "copy x");
+        return;
+    }
+    sfk::k_transform<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->y[c->cur]),
+                                                                    c->vol(out), c->st);
+    launched(c->stream, "k_transform");
+}
+
+void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
+                sfseg_iter_record* rec) {
+    validate_params(p);
+    if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_solve before sfseg_load");
+    if (first < 1 || last < first) fail(SFSEG_ERR_PARAMETER, "bad iteration range");
+    if (first > 1 && c->cur < 0) fail(SFSEG_ERR_STATE, "continuing a solve that never started");
+    const HostKernel k = make_kernel(p->radii, p->sigmas);
+    ensure_guard(c, !p->allow_negative_affinity);
+    ensure_sp(c, p->p);
+    const int n = last - first + 1;
+    if (c->norms_cap < n) {
+        if (c->norms) cudaFree(c->norms);
+        ck(cudaMalloc(&c->norms, n * sizeof(double)), "cudaMalloc norms");
+        c->norms_cap = n;
+    }
+    if (first == 1) {
+        IterState s{};
+        s.mode = 0;
+        set_state(c, c->st, s);
+        ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
+        c->cur = -1;
+    }
+    for (auto e : c->ev) cudaEventDestroy(e);
+    c->ev.clear();
+    std::vector<cudaEvent_t> iter_ev(n + 1);
+    for (auto& e : iter_ev) ck(cudaEventCreate(&e), "event");
+    ck(cudaEventRecord(iter_ev[0], c->stream), "event");
+    for (int it = first; it <= last; ++it) {
+        const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
+        const int dst = c->cur < 0 ? 0 : 1 - c->cur;
+        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->Fw);
+        const int mode_next = it >= p->binarize_start ? 2 : 1;
+        finalize(c, c->st, c->norms, it - first, mode_next, lambda_for(p, it), p->threshold_frac);
+        c->cur = dst;
+        ck(cudaEventRecord(iter_ev[it - first + 1], c->stream), "event");
+    }
+    std::vector<double> norms(n);
+    ck(cudaMemcpyAsync(norms.data(), c->norms, n * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream),
+       "norms");
+    ck(cudaStreamSynchronize(c->stream), "solve");
+    sfseg_timing tm{};
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, iter_ev[0], iter_ev[n]);
+    tm.solve_ms = ms;
+    for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
+        float m = 0.0f;
+        cudaEventElapsedTime(&m, c->ev[i], c->ev[i + 1]);
+        tm.step_kernel_ms += m;
+        ++tm.step_launches;
+    }
+    c->last_timing = tm;
+    for (int i = 0; i < n; ++i) {
+        if (rec) {
+            rec[i].iter = first + i;
+            rec[i].l2_norm_pre_normalize = norms[i];
+            rec[i].angle_deg = NAN;
+            rec[i].iou = NAN;
+            float m = 0.0f;
+            cudaEventElapsedTime(&m, iter_ev[i], iter_ev[i + 1]);
+            rec[i].wall_time_s = m * 1e-3;
+        }
+    }
+    for (auto e : iter_ev) cudaEventDestroy(e);
+    for (int i = 0; i < n; ++i)
+        if (norms[i] == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+}
+
+void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+               const float* const* F, const float* x0, int32_t mem) {
+    check_shape(T, H, W);
+    if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
+    if (!S || !F) fail(SFSEG_ERR_PARAMETER, "null input");
+    for (int i = 0; i < C; ++i)
+        if (!F[i]) fail(SFSEG_ERR_PARAMETER, "null pairwise channel");
+    set_shape(c, T, H, W, C);
+    // a fresh upload invalidates derived buffers
+    if (c->guard_applied)
+        for (size_t i = 0; i < c->Fw.size(); ++i)
+            if (c->Fw[i] != c->F[i]) dfree(c->Fw[i]);
+    c->Fw = c->F;
+    c->guard_applied = false;
+    c->sp_p = NAN;
+    c->cur = -1;
+    upload(c, c->S, S, mem);
+    for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
+    validate_vol(c, c->S, true, "unary");
+    for (int i = 0; i < C; ++i) validate_vol(c, c->F[i], false, "pairwise");
+    c->has_x0 = x0 != nullptr;
+    if (x0) {
+        if (!c->x0) c->x0 = dalloc_vol(c);
+        upload(c, c->x0, x0, mem);
+        validate_vol(c, c->x0, true, "x0");
+    }
+    c->resident = true;
+}
+
+// stateless helpers: (re)use the resident buffers of a scratch problem
+void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
+    check_shape(T, H, W);
+    set_shape(c, T, H, W, C);
+    c->guard_applied = false;
+    c->Fw = c->F;
+    c->sp_p = NAN;
+    c->cur = -1;
+    c->has_x0 = false;
+    c->resident = false;  // stateless operators reuse the resident buffers
+}
+
+void reduce_volume(sfseg_ctx* c, float* v, IterState* st, int mode_next, double lambda,
+                   double frac) {
+    ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
+    const long long warps = static_cast<long long>(c->T) * c->nbands() * c->nhalves();
+    sfk::k_partials<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, c->stream>>>(
+        c->vol(v), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
+    launched(c->stream, "k_partials");
+    finalize(c, st, nullptr, 0, mode_next, lambda, frac);
+}
+
+float* max_of(sfseg_ctx* c, float* v) {
+    ck(cudaMemsetAsync(c->scratch_f, 0, sizeof(float), c->stream), "memset");
+    sfk::k_max<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(v), c->scratch_f);
+    launched(c->stream, "k_max");
+    return c->scratch_f;
+}
+
+void mask_of(sfseg_ctx* c, float* v, double frac, uint8_t* mask, int32_t mem) {
+    float* mx = max_of(c, v);
+    const size_t n = static_cast<size_t>(c->T) * c->H * c->W;
+    uint8_t* dm = reinterpret_cast<uint8_t*>(mem == SFSEG_MEM_DEVICE ? mask : nullptr);
+    if (!dm) ck(cudaMallocAsync(reinterpret_cast<void**>(&dm), n, c->stream), "malloc mask");
+    sfk::k_mask<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(v), mx, frac, dm);
+    launched(c->stream, "k_mask");
+    if (mem != SFSEG_MEM_DEVICE) {
+        ck(cudaMemcpyAsync(mask, dm, n, cudaMemcpyDeviceToHost, c->stream), "mask D2H");
+        ck(cudaFreeAsync(dm, c->stream), "free");
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+void sfseg_params_default(sfseg_params* p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    p->alpha = 1.0;
+    p->p = 0.1;
+    p->radii[0] = 1;
+    p->radii[1] = 3;
+    p->radii[2] = 3;
+    p->sigmas[0] = 0.5;
+    p->sigmas[1] = 1.5;
+    p->sigmas[2] = 1.5;
+    p->iterations = 5;
+    p->temporal_window = -1;
+    p->binarize_start = 3;
+    p->sigmoid_slope0 = 10.0;
+    p->slope_growth = 2.0;
+    p->threshold_frac = 0.5;
+    p->final_threshold = 0.5;
+    p->allow_negative_affinity = 0;
+    p->arith = SFSEG_ARITH_EXACT;
+}
+
+int sfseg_params_validate(const sfseg_params* p) {
+    return guarded([&] { validate_params(p); });
+}
+
+int sfseg_make_kernel(const int32_t radii[3], const double sigmas[3], double* tt, double* ty,
+                      double* tx) {
+    return guarded([&] {
+        const HostKernel k = make_kernel(radii, sigmas);
+        std::memcpy(tt, k.t.data(), k.t.size() * sizeof(double));
+        std::memcpy(ty, k.y.data(), k.y.size() * sizeof(double));
+        std::memcpy(tx, k.x.data(), k.x.size() * sizeof(double));
+    });
+}
+
+const char* sfseg_last_error(void) { return g_err.c_str(); }
+
+const char* sfseg_build_info(void) {
+    return "sfseg_cuda abi=" "1" " arch=sm_100a fused=exact(rt,r)={(1,2),(1,3),(2,4),(2,5)}";
+}
+
+uint64_t sfseg_separable_convolution_count(void) {
+    return g_conv_count.load(std::memory_order_relaxed);
+}
+
+int sfseg_ctx_create(int device, sfseg_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(SFSEG_ERR_PARAMETER, "null out");
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(SFSEG_ERR_CUDA, "no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            fail(SFSEG_ERR_CUDA, std::string("sfseg_cuda is built for sm_100a; device is ") +
+                                     prop.name);
+        auto* c = new sfseg_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaMalloc(&c->st, sizeof(IterState)), "malloc");
+        ck(cudaMalloc(&c->st_aux, sizeof(IterState)), "malloc");
+        ck(cudaMalloc(&c->flags, sizeof(int)), "malloc");
+        ck(cudaMalloc(&c->scratch_f, 4 * sizeof(float)), "malloc");
+        ck(cudaMalloc(&c->bminmax, 2 * aux_grid(c) * sizeof(float)), "malloc");
+        ck(cudaMalloc(&c->acc3, 3 * sizeof(double)), "malloc");
+        ck(cudaMalloc(&c->cnt2, 2 * sizeof(unsigned long long)), "malloc");
+        *out = c;
+    });
+}
+
+int sfseg_ctx_destroy(sfseg_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        release_problem(c);
+        cudaFree(c->st);
+        cudaFree(c->st_aux);
+        cudaFree(c->flags);
+        cudaFree(c->scratch_f);
+        cudaFree(c->bminmax);
+        cudaFree(c->acc3);
+        cudaFree(c->cnt2);
+        if (c->norms) cudaFree(c->norms);
+        for (auto e : c->ev) cudaEventDestroy(e);
+        cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int sfseg_ctx_set_timing(sfseg_ctx* c, int enabled) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        c->timing = enabled != 0;
+    });
+}
+
+int sfseg_ctx_get_timing(const sfseg_ctx* c, sfseg_timing* out) {
+    return guarded([&] {
+        if (!c || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        *out = c->last_timing;
+    });
+}
+
+int sfseg_ctx_synchronize(sfseg_ctx* c) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int sfseg_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+               const float* const* F, const float* x0, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        load_impl(c, T, H, W, C, S, F, x0, mem);
+    });
+}
+
+int sfseg_solve(sfseg_ctx* c, const sfseg_params* p, int32_t first, int32_t last,
+                sfseg_iter_record* rec) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        solve_impl(c, p, first, last, rec);
+    });
+}
+
+int sfseg_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_download before sfseg_load");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        float* x = tmp_vol(c, 0);
+        materialize(c, x);
+        if (soft) download(c, soft, x, mem);
+        if (mask) mask_of(c, x, frac, mask, mem);
+        ck(cudaStreamSynchronize(c->stream), "download");
+    });
+}
+
+int sfseg_metrics(sfseg_ctx* c, const float* reference, const uint8_t* gt, double frac,
+                  double* angle, double* iou, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_metrics before sfseg_load");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        float* x = tmp_vol(c, 0);
+        materialize(c, x);
+        Vol ref{nullptr, c->T, c->H, c->W, c->P};
+        if (reference) {
+            ref.p = tmp_vol(c, 1);
+            upload(c, ref.p, reference, mem);
+        }
+        const size_t n = static_cast<size_t>(c->T) * c->H * c->W;
+        uint8_t* dgt = nullptr;
+        if (gt) {
+            ck(cudaMallocAsync(reinterpret_cast<void**>(&dgt), n, c->stream), "malloc");
+            ck(cudaMemcpyAsync(dgt, gt, n,
+                               mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                       : cudaMemcpyHostToDevice,
+                               c->stream),
+               "gt");
+        }
+        float* mx = gt ? max_of(c, x) : nullptr;
+        ck(cudaMemsetAsync(c->acc3, 0, 3 * sizeof(double), c->stream), "memset");
+        ck(cudaMemsetAsync(c->cnt2, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
+        sfk::k_metrics<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(x), ref, dgt, mx,
+                                                                      frac, c->acc3, c->cnt2);
+        launched(c->stream, "k_metrics");
+        double a3[3];
+        unsigned long long c2[2];
+        ck(cudaMemcpyAsync(a3, c->acc3, sizeof a3, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaMemcpyAsync(c2, c->cnt2, sizeof c2, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (dgt) ck(cudaFreeAsync(dgt, c->stream), "free");
+        ck(cudaStreamSynchronize(c->stream), "metrics");
+        if (angle) {
+            if (!reference) {
+                *angle = NAN;
+            } else {
+                if (a3[1] == 0.0 || a3[2] == 0.0)
+                    fail(SFSEG_ERR_PARAMETER, "angle is undefined for a zero vector");
+                const double cs =
+                    std::clamp(a3[0] / (std::sqrt(a3[1]) * std::sqrt(a3[2])), -1.0, 1.0);
+                *angle = std::acos(cs) * 57.295779513082320876798154814105;
+            }
+        }
+        if (iou) *iou = !gt ? NAN : (c2[1] == 0 ? 1.0 : double(c2[0]) / double(c2[1]));
+    });
+}
+
+int sfseg_run(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+              const float* const* F, const float* x0, const sfseg_params* p, float* soft,
+              uint8_t* mask, sfseg_iter_record* rec, int32_t mem) {
+    int rc = sfseg_params_validate(p);
+    if (rc) return rc;
+    rc = sfseg_load(c, T, H, W, C, S, F, x0, mem);
+    if (rc) return rc;
+    rc = sfseg_solve(c, p, 1, p->iterations, rec);
+    if (rc) return rc;
+    return sfseg_download(c, p->final_threshold, soft, mask, mem);
+}
+
+int sfseg_step(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* x,
+               const float* S, const float* const* F, const sfseg_params* p, float* out,
+               int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        validate_params(p);  // engine.cpp:143
+        if (C < 1) fail(SFSEG_ERR_PARAMETER, "sfseg_step needs at least one pairwise channel");
+        if (!x || !S || !F || !out) fail(SFSEG_ERR_PARAMETER, "null input");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const HostKernel k = make_kernel(p->radii, p->sigmas);
+        stage_volume(c, T, H, W, C);
+        upload(c, c->S, S, mem);
+        for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
+        float* xin = c->y[1];
+        upload(c, xin, x, mem);
+        ensure_sp(c, p->p);
+        IterState s{};
+        s.mode = 0;
+        set_state(c, c->st_aux, s);
+        ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
+        launch_step(c, k, p->alpha, xin, c->st_aux, c->y[0], c->F);
+        download(c, out, c->y[0], mem);
+        ck(cudaStreamSynchronize(c->stream), "sfseg_step");
+        c->sp_p = NAN;  // S is scratch now
+    });
+}
+
+int sfseg_step_channel(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+                       const float* S, const float* f, const sfseg_params* p, float* out,
+                       int32_t mem) {
+    const float* F[1] = {f};
+    return sfseg_step(c, T, H, W, 1, x, S, F, p, out, mem);
+}
+
+int sfseg_normalize_l2(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+                       float* out, double* norm, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        if (!x) fail(SFSEG_ERR_PARAMETER, "null input");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        float* v = c->y[0];
+        upload(c, v, x, mem);
+        IterState s{};
+        set_state(c, c->st_aux, s);
+        reduce_volume(c, v, c->st_aux, 1, 0.0, 0.5);
+        const IterState r = get_state(c, c->st_aux);
+        if (norm) *norm = r.norm;
+        if (r.norm == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+        if (out) {
+            sfk::k_transform<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(
+                c->vol(v), c->vol(c->y[1]), c->st_aux);
+            launched(c->stream, "k_transform");
+            download(c, out, c->y[1], mem);
+            ck(cudaStreamSynchronize(c->stream), "normalize_l2");
+        }
+    });
+}
+
+int sfseg_project_binary(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+                         int32_t iter, const sfseg_params* p, float* out, int32_t mem) {
+    return guarded([&] {
+        if (!c || !p || !x || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        float* v = c->y[0];
+        upload(c, v, x, mem);
+        if (iter < p->binarize_start) {  // engine.cpp:186
+            download(c, out, v, mem);
+            ck(cudaStreamSynchronize(c->stream), "project_binary");
+            return;
+        }
+        float* mx = max_of(c, v);
+        float hmax = 0.0f;
+        ck(cudaMemcpyAsync(&hmax, mx, sizeof hmax, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        IterState s{};
+        s.mode = 2;
+        s.inv = 1.0;  // float(double(x) * 1.0) == x exactly
+        s.theta = p->threshold_frac * static_cast<double>(hmax);
+        s.lambda = lambda_for(p, iter);
+        set_state(c, c->st_aux, s);
+        sfk::k_transform<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(
+            c->vol(v), c->vol(c->y[1]), c->st_aux);
+        launched(c->stream, "k_transform");
+        download(c, out, c->y[1], mem);
+        ck(cudaStreamSynchronize(c->stream), "project_binary");
+    });
+}
+
+int sfseg_threshold_final(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+                          double frac, uint8_t* mask, int32_t mem) {
+    return guarded([&] {
+        if (!c || !x || !mask) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        float* v = c->y[0];
+        upload(c, v, x, mem);
+        mask_of(c, v, frac, mask, mem);
+        ck(cudaStreamSynchronize(c->stream), "threshold_final");
+    });
+}
+
+int sfseg_convolve_separable(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* v,
+                             const int32_t radii[3], const double sigmas[3], float* out,
+                             int32_t mem) {
+    return guarded([&] {
+        if (!c || !v || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const HostKernel k = make_kernel(radii, sigmas);
+        if (k.rt > 31 || k.ry > 31 || k.rx > 31) fail(SFSEG_ERR_CAPACITY, "kernel radius above 31");
+        stage_volume(c, T, H, W, 1);
+        sfk::Taps tp;
+        std::memset(&tp, 0, sizeof tp);
+        for (int i = 0; i <= 2 * k.rt; ++i) tp.t[i] = static_cast<float>(k.t[i]);
+        for (int i = 0; i <= 2 * k.ry; ++i) tp.y[i] = static_cast<float>(k.y[i]);
+        for (int i = 0; i <= 2 * k.rx; ++i) tp.x[i] = static_cast<float>(k.x[i]);
+        tp.rt = k.rt;
+        tp.ry = k.ry;
+        tp.rx = k.rx;
+        float *a = c->y[0], *b = c->y[1], *t0 = tmp_vol(c, 0);
+        upload(c, a, v, mem);
+        const int g = aux_grid(c), bt = sfk::kAuxThreads;
+        sfk::k_pass_x<<<g, bt, 0, c->stream>>>(c->vol(a), c->vol(t0), tp);
+        sfk::k_pass_y<<<g, bt, 0, c->stream>>>(c->vol(t0), c->vol(b), tp);
+        sfk::k_pass_t<<<g, bt, 0, c->stream>>>(c->vol(b), c->vol(a), tp);
+        launched(c->stream, "convolve_separable");
+        download(c, out, a, mem);
+        ck(cudaStreamSynchronize(c->stream), "convolve_separable");
+        g_conv_count.fetch_add(1, std::memory_order_relaxed);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// sfseg_types.cuh — structures shared between the host driver and kernels.
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+namespace sfk {
+
+constexpr int kMaxCG = 4;      // feature channels fused into one stencil pass
+constexpr int kMaxTapsXY = 32;  // 2*R+1 for R <= 15
+constexpr int kMaxTapsT = 16;   // 2*RT+1 for RT <= 7
+
+// Scalars carried from one iteration to the next, written on the device by
+// finalize_total and read by the next stencil launch (no host round trip).
+struct IterState {
+    double inv;        // 1 / ||y_k||                      (engine.cpp:178)
+    double theta;      // threshold_frac * max(x_unit)     (engine.cpp:191)
+    double lambda;     // slope0 * growth^(k - start)      (engine.cpp:192-193)
+    double norm;       // ||y_k||
+    int32_t mode;      // 0: x = y (iteration 1); 1: normalise; 2: normalise + sigmoid
+    int32_t degenerate;  // sticky: some ||y_k|| == 0      (engine.cpp:174-175)
+    float max_raw;     // max(0, max y_k)
+    float max_unit;    // max(0, max x_unit)
+};
+
+// Arguments of one fused stencil launch (one channel group of one step).
+struct FusedArgs {
+    CUtensorMap tm_x;           // iterate source y_k (or S / x0 at iteration 1)
+    CUtensorMap tm_sp;          // S^p
+    CUtensorMap tm_f[kMaxCG];   // feature channels of this group
+    const float* sp;            // pitched S^p (recombination reload)
+    const float* f[kMaxCG];
+    float* out;                 // pitched y_{k+1}
+    double* part;               // canonical partial sums [T][nbands][nhalves]
+    float* frame_max;           // [T] max(0, y_{k+1}) per frame (int-ordered)
+    const IterState* st;
+    float taps_x[kMaxTapsXY];
+    float taps_y[kMaxTapsXY];
+    float taps_t[kMaxTapsT];
+    float inv_alpha;
+    int T, H, W, pitch;
+    int buf_t0;      // global frame of input buffer frame 0
+    int out_t0, out_t1;  // global output frames [out_t0, out_t1)
+    int out_buf_t0;  // global frame of output buffer frame 0
+    int tiles_x, tiles_y;
+    long long units_per_cta;
+    int first_group, last_group;
+    int nbands, nhalves;
+};
+
+}  // namespace sfk

@@ -1,0 +1,487 @@
+"""Python mirror of the reference solve API (proj/include/sfseg/engine.hpp).
+
+Same names, argument meaning and error behaviour as the C++ reference:
+
+=====================  ===========================================
+reference (C++)         here
+=====================  ===========================================
+SfsegConfig             SfsegConfig (engine.hpp:22-57)
+KernelConfig            KernelConfig (conv3d.hpp:20-23)
+sfseg_step_channel      sfseg_step_channel (engine.hpp:63-64)
+sfseg_step              sfseg_step (engine.hpp:67-68)
+normalize_l2            normalize_l2 (engine.hpp:72)
+project_binary          project_binary (engine.hpp:78)
+threshold_final         threshold_final (engine.hpp:82)
+run                     run (engine.hpp:104-109)
+make_gaussian_kernel    make_gaussian_kernel (conv3d.hpp:55-57)
+convolve_separable      convolve_separable (conv3d.hpp:62-63)
+=====================  ===========================================
+
+Volumes are float32 arrays of shape (T, H, W) in the reference's linear order
+(volume.hpp:32-36): numpy arrays (host memory) or CUDA torch tensors (device
+memory, used in place). Every call goes through the C ABI in
+include/sfseg_cuda.h to the sm_100a kernels; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import (CapacityError, DegenerateSolutionError, Error, ParameterError,
+                      ShapeError, ValidationError)
+
+__all__ = [
+    "KernelConfig", "SfsegConfig", "FeatureSet", "IterationRecord", "RunTrace", "RunResult",
+    "SeparableKernel3D", "make_gaussian_kernel", "convolve_separable", "sfseg_step",
+    "sfseg_step_channel", "normalize_l2", "project_binary", "threshold_final", "run",
+    "separable_convolution_count", "Context", "default_context", "Error", "ParameterError",
+    "ShapeError", "ValidationError", "DegenerateSolutionError", "CapacityError",
+]
+
+ARITH_EXACT = N.SFSEG_ARITH_EXACT
+ARITH_FAST = N.SFSEG_ARITH_FAST
+
+
+@dataclass
+class KernelConfig:
+    """Per-axis radii/sigmas, axis order (t, y, x) (conv3d.hpp:20-23)."""
+
+    radii: tuple = (1, 3, 3)
+    sigmas: tuple = (0.5, 1.5, 1.5)
+
+
+@dataclass
+class SfsegConfig:
+    """Solver configuration; defaults of engine.hpp:22-49.
+
+    ``arith`` selects the kernel arithmetic (not in the reference): "exact"
+    reproduces the reference's rounding order bit for bit; "fast" uses fused
+    multiply-adds (within the north-star tolerance). Default: $SFSEG_ARITH or
+    "exact". ``threads`` is accepted and ignored, as on the GPU it has no
+    meaning (README.md:174-189 makes results thread-count invariant).
+    """
+
+    alpha: float = 1.0
+    p: float = 0.1
+    kernel: KernelConfig = field(default_factory=KernelConfig)
+    iterations: int = 5
+    temporal_window: int = -1
+    binarize_start: int = 3
+    sigmoid_slope0: float = 10.0
+    slope_growth: float = 2.0
+    threshold_frac: float = 0.5
+    final_threshold: float = 0.5
+    allow_negative_affinity: bool = False
+    threads: int = 0
+    arith: str = field(default_factory=lambda: os.environ.get("SFSEG_ARITH", "exact"))
+
+    def resolved_temporal_window(self) -> int:
+        return self.kernel.radii[0] if self.temporal_window < 0 else self.temporal_window
+
+    def to_params(self) -> N.Params:
+        p = N.Params()
+        p.alpha = float(self.alpha)
+        p.p = float(self.p)
+        for a in range(3):
+            p.radii[a] = int(self.kernel.radii[a])
+            p.sigmas[a] = float(self.kernel.sigmas[a])
+        p.iterations = int(self.iterations)
+        p.temporal_window = int(self.temporal_window)
+        p.binarize_start = int(self.binarize_start)
+        p.sigmoid_slope0 = float(self.sigmoid_slope0)
+        p.slope_growth = float(self.slope_growth)
+        p.threshold_frac = float(self.threshold_frac)
+        p.final_threshold = float(self.final_threshold)
+        p.allow_negative_affinity = int(bool(self.allow_negative_affinity))
+        if self.arith not in ("exact", "fast"):
+            raise ParameterError("arith must be 'exact' or 'fast'")
+        p.arith = ARITH_EXACT if self.arith == "exact" else ARITH_FAST
+        return p
+
+    def validate(self) -> None:
+        """SfsegConfig::validate (engine.cpp:21-42); raises ParameterError."""
+        lib = N.load_library()
+        p = self.to_params()
+        N.check(lib.sfseg_params_validate(C.byref(p)))
+
+
+@dataclass
+class FeatureSet:
+    """Unary S plus >= 1 pairwise channels, all (T, H, W) (volume.hpp:90-96)."""
+
+    unary: object
+    pairwise: list
+
+    def shape(self):
+        return tuple(self.unary.shape)
+
+
+@dataclass
+class IterationRecord:
+    iter: int
+    l2_norm_pre_normalize: float
+    angle_deg: Optional[float] = None
+    iou: Optional[float] = None
+    wall_time_s: float = 0.0
+
+
+@dataclass
+class RunTrace:
+    iterations: list = field(default_factory=list)
+
+
+@dataclass
+class RunResult:
+    soft: np.ndarray
+    mask: np.ndarray
+    trace: RunTrace
+
+
+@dataclass
+class SeparableKernel3D:
+    taps_t: np.ndarray
+    taps_y: np.ndarray
+    taps_x: np.ndarray
+    radii: tuple
+    sigmas: tuple
+
+    def tap_count(self) -> int:
+        return len(self.taps_t) + len(self.taps_y) + len(self.taps_x)
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One CUDA device + stream + resident buffers (sfseg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.load_library()
+        h = C.c_void_p()
+        N.check(self._lib.sfseg_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+        self.lock = threading.Lock()
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.sfseg_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, on: bool) -> None:
+        N.check(self._lib.sfseg_ctx_set_timing(self.handle, int(on)))
+
+    def timing(self) -> N.Timing:
+        t = N.Timing()
+        N.check(self._lib.sfseg_ctx_get_timing(self.handle, C.byref(t)))
+        return t
+
+    def synchronize(self) -> None:
+        N.check(self._lib.sfseg_ctx_synchronize(self.handle))
+
+
+_ctx_lock = threading.Lock()
+_contexts: dict = {}
+
+
+def default_context(device: Optional[int] = None) -> Context:
+    if device is None:
+        device = int(os.environ.get("SFSEG_DEVICE", "0"))
+    with _ctx_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _contexts[device] = ctx
+        return ctx
+
+
+def _is_torch_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(getattr(a, "is_cuda"))
+
+
+class _Buf:
+    """A volume argument as (pointer, mem kind), keeping host copies alive."""
+
+    def __init__(self, a, shape=None, writable=False, dtype=np.float32):
+        if _is_torch_cuda(a):
+            import torch
+
+            want = torch.float32 if dtype == np.float32 else torch.uint8
+            if a.dtype != want or not a.is_contiguous():
+                raise ValidationError("device volumes must be contiguous " + str(want))
+            self.arr = a
+            self.ptr = C.c_void_p(a.data_ptr())
+            self.mem = N.SFSEG_MEM_DEVICE
+            self.shape = tuple(a.shape)
+        else:
+            arr = np.asarray(a)
+            if arr.dtype != dtype or not arr.flags.c_contiguous:
+                if writable:
+                    raise ValidationError("output buffer must be a contiguous %s array" % dtype)
+                arr = np.ascontiguousarray(arr, dtype=dtype)
+            self.arr = arr
+            self.ptr = C.c_void_p(arr.ctypes.data)
+            self.mem = N.SFSEG_MEM_HOST
+            self.shape = tuple(arr.shape)
+        if shape is not None and self.shape != tuple(shape):
+            raise ShapeError("shape mismatch: %s vs %s" % (self.shape, tuple(shape)))
+
+
+def _shape3(shape) -> tuple:
+    if len(shape) != 3:
+        raise ShapeError("volumes are (T, H, W)")
+    return tuple(int(s) for s in shape)
+
+
+def _empty_like(buf: _Buf, dtype=np.float32):
+    if buf.mem == N.SFSEG_MEM_DEVICE:
+        import torch
+
+        return torch.empty(buf.shape, dtype=torch.float32 if dtype == np.float32 else torch.uint8,
+                           device=buf.arr.device)
+    return np.empty(buf.shape, dtype=dtype)
+
+
+def _same_mem(bufs: Sequence[_Buf]) -> int:
+    kinds = {b.mem for b in bufs}
+    if len(kinds) != 1:
+        raise ValidationError("mixing host and device volumes in one call")
+    return kinds.pop()
+
+
+# ---------------------------------------------------------------------------
+def make_gaussian_kernel(sigmas, radii) -> SeparableKernel3D:
+    """make_gaussian_kernel (conv3d.cpp:40-58); fp64 taps, mass folded into taps_t."""
+    lib = N.load_library()
+    r = (C.c_int32 * 3)(*[int(v) for v in radii])
+    s = (C.c_double * 3)(*[float(v) for v in sigmas])
+    if any(v < 0 for v in radii):
+        raise ParameterError("kernel radius must be nonnegative")
+    tt = np.zeros(2 * int(radii[0]) + 1)
+    ty = np.zeros(2 * int(radii[1]) + 1)
+    tx = np.zeros(2 * int(radii[2]) + 1)
+    dp = C.POINTER(C.c_double)
+    N.check(lib.sfseg_make_kernel(r, s, tt.ctypes.data_as(dp), ty.ctypes.data_as(dp),
+                                  tx.ctypes.data_as(dp)))
+    return SeparableKernel3D(tt, ty, tx, tuple(radii), tuple(sigmas))
+
+
+def convolve_separable(v, kernel: KernelConfig | SeparableKernel3D, threads: int = 1,
+                       ctx: Optional[Context] = None):
+    """convolve_separable (conv3d.cpp:171-185): x, y then t pass, zero padded."""
+    ctx = ctx or default_context()
+    b = _Buf(v)
+    T, H, W = _shape3(b.shape)
+    out = _empty_like(b)
+    ob = _Buf(out, writable=True)
+    r = (C.c_int32 * 3)(*[int(x) for x in kernel.radii])
+    s = (C.c_double * 3)(*[float(x) for x in kernel.sigmas])
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_convolve_separable(ctx.handle, T, H, W, b.ptr, r, s, ob.ptr, b.mem))
+    return out
+
+
+def separable_convolution_count() -> int:
+    """separable_convolution_count (conv3d.cpp:64-66), counted by this library."""
+    return int(N.load_library().sfseg_separable_convolution_count())
+
+
+def _channel_ptrs(bufs: Sequence[_Buf]):
+    arr = (C.c_void_p * len(bufs))(*[b.ptr.value for b in bufs])
+    return arr
+
+
+def sfseg_step(x, features: FeatureSet, cfg: SfsegConfig, ctx: Optional[Context] = None):
+    """sfseg_step (engine.cpp:141-166): sum of per-channel steps, unnormalised."""
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    if len(features.pairwise) == 0:
+        raise ParameterError("sfseg_step needs at least one pairwise channel")
+    xb = _Buf(x)
+    shape = _shape3(xb.shape)
+    try:
+        sb = _Buf(features.unary, shape)
+    except ShapeError:
+        raise ShapeError("shape mismatch: solution vs unary")
+    fbs = []
+    for f in features.pairwise:
+        try:
+            fbs.append(_Buf(f, shape))
+        except ShapeError:
+            raise ShapeError("shape mismatch: solution vs pairwise")
+    mem = _same_mem([xb, sb] + fbs)
+    out = _empty_like(xb)
+    ob = _Buf(out, writable=True)
+    T, H, W = shape
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_step(ctx.handle, T, H, W, len(fbs), xb.ptr, sb.ptr,
+                                    C.cast(_channel_ptrs(fbs), C.c_void_p), C.byref(p), ob.ptr, mem))
+    return out
+
+
+def sfseg_step_channel(x, s, f, cfg: SfsegConfig, ctx: Optional[Context] = None):
+    """sfseg_step_channel (engine.cpp:131-139)."""
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    xb = _Buf(x)
+    shape = _shape3(xb.shape)
+    try:
+        sb = _Buf(s, shape)
+    except ShapeError:
+        raise ShapeError("shape mismatch: solution vs unary")
+    try:
+        fb = _Buf(f, shape)
+    except ShapeError:
+        raise ShapeError("shape mismatch: solution vs pairwise")
+    mem = _same_mem([xb, sb, fb])
+    out = _empty_like(xb)
+    ob = _Buf(out, writable=True)
+    T, H, W = shape
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_step_channel(ctx.handle, T, H, W, xb.ptr, sb.ptr, fb.ptr,
+                                            C.byref(p), ob.ptr, mem))
+    return out
+
+
+def normalize_l2(x, ctx: Optional[Context] = None):
+    """normalize_l2 (engine.cpp:168-183) -> (unit volume, norm)."""
+    ctx = ctx or default_context()
+    xb = _Buf(x)
+    T, H, W = _shape3(xb.shape)
+    out = _empty_like(xb)
+    ob = _Buf(out, writable=True)
+    norm = C.c_double()
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_normalize_l2(ctx.handle, T, H, W, xb.ptr, ob.ptr, C.byref(norm),
+                                            xb.mem))
+    return out, norm.value
+
+
+def project_binary(x, it: int, cfg: SfsegConfig, ctx: Optional[Context] = None):
+    """project_binary (engine.cpp:185-205)."""
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    xb = _Buf(x)
+    T, H, W = _shape3(xb.shape)
+    out = _empty_like(xb)
+    ob = _Buf(out, writable=True)
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_project_binary(ctx.handle, T, H, W, xb.ptr, int(it), C.byref(p),
+                                              ob.ptr, xb.mem))
+    return out
+
+
+def threshold_final(x, frac: float, ctx: Optional[Context] = None):
+    """threshold_final (engine.cpp:207-214): uint8 mask of x > float(frac*max)."""
+    ctx = ctx or default_context()
+    xb = _Buf(x)
+    T, H, W = _shape3(xb.shape)
+    out = _empty_like(xb, np.uint8)
+    ob = _Buf(out, writable=True, dtype=np.uint8)
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_threshold_final(ctx.handle, T, H, W, xb.ptr, float(frac), ob.ptr,
+                                               xb.mem))
+    return out
+
+
+IterationObserver = Callable[[int, np.ndarray], None]
+
+
+def run(features: FeatureSet, cfg: SfsegConfig, x0=None, reference=None, ground_truth=None,
+        transform=None, observer: Optional[IterationObserver] = None,
+        ctx: Optional[Context] = None) -> RunResult:
+    """sfseg::run (engine.cpp:247-348) on the GPU.
+
+    The per-frame windowed sweep of the reference is replaced by one global
+    step per iteration (bit-equal, test_engine.cpp:276-297). ``transform``
+    (FrameTransform) is supported only as None: a non-empty hook needs the
+    windowed host round trip and lives in the C++ drop-in shim.
+    """
+    if transform is not None:
+        raise ParameterError("FrameTransform hooks are handled by the C++ drop-in shim")
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    sb = _Buf(features.unary)
+    shape = _shape3(sb.shape)
+    if len(features.pairwise) == 0:
+        raise ValidationError("feature set needs at least one pairwise channel")
+    fbs = []
+    for f in features.pairwise:
+        try:
+            fbs.append(_Buf(f, shape))
+        except ShapeError:
+            raise ShapeError("pairwise channel shape differs from unary shape")
+    bufs = [sb] + fbs
+    x0b = None
+    if x0 is not None:
+        try:
+            x0b = _Buf(x0, shape)
+        except ShapeError:
+            raise ShapeError("x0 shape differs from features")
+        bufs.append(x0b)
+    refb = gtb = None
+    if reference is not None:
+        try:
+            refb = _Buf(reference, shape)
+        except ShapeError:
+            raise ShapeError("reference shape differs from features")
+    if ground_truth is not None:
+        try:
+            gtb = _Buf(ground_truth, shape, dtype=np.uint8)
+        except ShapeError:
+            raise ShapeError("ground truth shape differs from features")
+    mem = _same_mem(bufs)
+    T, H, W = shape
+    lib = ctx._lib
+    soft = _empty_like(sb)
+    mask = _empty_like(sb, np.uint8)
+    trace = RunTrace()
+    with ctx.lock:
+        N.check(lib.sfseg_load(ctx.handle, T, H, W, len(fbs), sb.ptr,
+                               C.cast(_channel_ptrs(fbs), C.c_void_p),
+                               x0b.ptr if x0b else None, mem))
+        per_iter = observer is not None or refb is not None or gtb is not None
+        if not per_iter:
+            recs = (N.IterRecord * cfg.iterations)()
+            N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, cfg.iterations, recs))
+            for r in recs:
+                trace.iterations.append(IterationRecord(r.iter, r.l2_norm_pre_normalize,
+                                                        wall_time_s=r.wall_time_s))
+        else:
+            x_it = _empty_like(sb)
+            xib = _Buf(x_it, writable=True)
+            for it in range(1, cfg.iterations + 1):
+                rec = N.IterRecord()
+                N.check(lib.sfseg_solve(ctx.handle, C.byref(p), it, it, C.byref(rec)))
+                r = IterationRecord(rec.iter, rec.l2_norm_pre_normalize,
+                                    wall_time_s=rec.wall_time_s)
+                if refb is not None or gtb is not None:
+                    ang, iou = C.c_double(), C.c_double()
+                    N.check(lib.sfseg_metrics(ctx.handle, refb.ptr if refb else None,
+                                              gtb.ptr if gtb else None, float(cfg.threshold_frac),
+                                              C.byref(ang), C.byref(iou), mem))
+                    if refb is not None:
+                        r.angle_deg = ang.value
+                    if gtb is not None:
+                        r.iou = iou.value
+                trace.iterations.append(r)
+                if observer is not None:
+                    N.check(lib.sfseg_download(ctx.handle, 0.5, xib.ptr, None, mem))
+                    observer(it, x_it)
+        ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
+        N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold), ob.ptr, mb.ptr, mem))
+    return RunResult(soft, mask, trace)
