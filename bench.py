@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""SFSeg power-iteration benchmark (BASELINE.json metric: voxel-iterations/s,
+achieved HBM GB/s vs roofline).
+
+Workload (default): BASELINE.json configs[1] — T=80, H=480, W=854, C=1,
+kernel 5x11x11 (radii 2,5,5; sigmas 0.5,1.5,1.5), 30 power iterations,
+alpha=1, p=0.1, binarisation off (pure power iteration). One bench "step" is
+one full solve: 30 iterations over the whole volume.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). ``value`` is device-resident throughput (inputs
+already in HBM, CUDA events on the library's launch stream, max over ranks);
+``e2e`` is the same metric through the public C ABI call sfseg_run with pinned
+host buffers (H2D of S and F, solve, D2H of the soft iterate and mask inside
+the timed region). ``--impl reference`` times the reference's own CPU
+implementation (oracle/_ref/libsfseg_ref.so, compiled from the reference
+sources) on the host cores with a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "voxel-iterations/s of SFSeg power iteration"
+UNIT = "voxel-iter/s"
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def reference_cpu(problem, iterations, frames, threads, reps=1):
+    """Reference CPU run() on a T-cropped sample of the workload."""
+    from tests.oracle_lib import Reference
+
+    ref = Reference()
+    T, H, W = problem.shape
+    from paper_1907_02731_b200 import synth
+
+    sample = synth.config(1, frames=frames)[0]
+    fs, _ = sample.generate()
+    cfg = sample.cfg
+    cfg.iterations = iterations
+    cfg.binarize_start = iterations + 1
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ref.run(fs.unary, fs.pairwise, cfg, threads=threads)
+        times.append(time.perf_counter() - t0)
+    vox = frames * H * W * iterations
+    return vox, times
+
+
+def run_reference_arm(args):
+    from paper_1907_02731_b200 import synth
+
+    prob = synth.config(args.config)[0]
+    threads = os.cpu_count() or 1
+    frames = args.ref_frames
+    iters = prob.cfg.iterations
+    vox = None
+    times = []
+    for i in range(args.warmup + args.steps):
+        vox, t = reference_cpu(prob, iters, frames, threads)
+        if i >= args.warmup:
+            times.extend(t)
+    total = sum(times)
+    value = vox * len(times) / total
+    T, H, W = prob.shape
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"BASELINE configs[{args.config}] ({prob.name}) T-cropped to "
+                               f"{frames} frames for the CPU", "shape": [frames, H, W],
+                   "channels": prob.channels, "radii": list(prob.cfg.kernel.radii),
+                   "sigmas": list(prob.cfg.kernel.sigmas), "iterations": iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"sfseg_ref::run on {frames}x{H}x{W}, C={prob.channels}, "
+                                   f"{iters} iterations per step, cfg.threads={threads}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--arith", default=os.environ.get("SFSEG_ARITH", "exact"),
+                    choices=["exact", "fast"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-frames", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1907_02731_b200 import _native as N
+    from paper_1907_02731_b200 import engine as E
+    from paper_1907_02731_b200 import synth
+
+    prob = synth.config(args.config)[0]
+    cfg = prob.cfg
+    cfg.arith = args.arith
+    T, H, W = prob.shape
+    Cn = prob.channels
+    nvox = T * H * W
+    iters = cfg.iterations
+
+    # pinned host inputs, generated once
+    S = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
+    F = [torch.empty((T, H, W), dtype=torch.float32, pin_memory=True) for _ in range(Cn)]
+    prob.generate(out=(S.numpy(), [f.numpy() for f in F]))
+
+    ctx = E.Context(local)
+    lib = ctx._lib
+    p = cfg.to_params()
+    fptrs = (C.c_void_p * Cn)(*[f.data_ptr() for f in F])
+    # device-resident load (H2D once, outside the timed region)
+    N.check(lib.sfseg_load(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
+                           C.cast(fptrs, C.c_void_p), None, N.SFSEG_MEM_HOST))
+
+    def barrier():
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
+    ctx.set_timing(True)
+    barrier()
+    solve_ms, kern_ms, launches = [], 0.0, 0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
+            tm = ctx.timing()
+            solve_ms.append(tm.solve_ms)
+            kern_ms += tm.step_kernel_ms
+            launches += tm.step_launches
+    barrier()
+    ctx.set_timing(False)
+    total_ms = sum(solve_ms)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * nvox * iters * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (fused stencil): algorithmic bytes per
+    # launch = 4 B x (x, S^p, F_c reads + one write) per voxel
+    bytes_per_launch = 4.0 * (Cn + 3) * nvox if Cn == 1 else 4.0 * (4) * nvox
+    avg_launch_ms = kern_ms / max(1, launches)
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    traffic = None
+    tfile = ROOT / "profiles" / f"traffic_c{args.config}_{args.arith}.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+
+    # end to end: public C ABI sfseg_run from pinned host memory, per step
+    soft = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
+    mask = torch.empty((T, H, W), dtype=torch.uint8, pin_memory=True)
+    e2e_t = []
+    for i in range(args.e2e_steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        N.check(lib.sfseg_run(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
+                              C.cast(fptrs, C.c_void_p), None, C.byref(p),
+                              C.c_void_p(soft.data_ptr()), C.c_void_p(mask.data_ptr()), None,
+                              N.SFSEG_MEM_HOST))
+        if i > 0:  # first call warms the path
+            e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * nvox * iters / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            vox, times = reference_cpu(prob, iters, args.ref_frames, threads)
+            cpu = {"value": vox / times[0], "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"sfseg_ref::run (reference compiled from its sources) on "
+                             f"{args.ref_frames}x{H}x{W}, C={Cn}, {iters} iterations, "
+                             f"cfg.threads={threads}; {times[0]:.1f} s"}
+        except Exception as e:  # the reference build may be absent
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE configs[{args.config}] ({prob.name})",
+                       "shape": [T, H, W], "channels": Cn, "radii": list(cfg.kernel.radii),
+                       "sigmas": list(cfg.kernel.sigmas), "iterations": iters,
+                       "alpha": cfg.alpha, "p": cfg.p, "binarization": "off",
+                       "arith": args.arith,
+                       "l2": f"inputs larger than L2 ({(Cn + 2) * nvox * 4 / 1e6:.0f} MB read per iteration)",
+                       "parallelism": f"replicas{world}" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                         "kernel": "fused_step_exact", "avg_launch_ms": avg_launch_ms,
+                         "bytes_per_launch": bytes_per_launch},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": (1 + Cn) * nvox * 4,
+                    "d2h_bytes_per_step": nvox * 4 + nvox},
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps * iters * (Cn + 2),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,14 +151,16 @@ def test_run_c0_matches_reference(binarize):
 def test_run_c1_cropped_matches_reference():
     prob, fs, _ = _problem(1, frames=10)
     cfg = prob.cfg
-    res = E.run(fs, cfg)
-    soft, mask, norms, _ = Oracle().run(fs.unary, fs.pairwise, cfg)
-    err, cos = _gate(res.soft, soft, "c1[T=10]")
+    snaps = {}
+    res = E.run(fs, cfg, observer=lambda it, x: snaps.__setitem__(it, x.copy()) if it == 1 else None)
+    soft, mask, norms, ck = Oracle().run(fs.unary, fs.pairwise, cfg, checkpoints=[1])
+    _gate(res.soft, soft, "c1[T=10]")
     _mask_gate(res.mask, mask, soft, cfg.final_threshold)
-    # exact arithmetic: the iterates stay bit-identical except where the fp64
-    # norm summation order differs in the last bit
-    frac_equal = np.mean(res.soft == soft)
-    assert frac_equal > 0.99, frac_equal
+    # exact arithmetic: after one iteration the iterate is bit-identical except
+    # where float(y * inv) rounds differently because the fp64 norm was summed
+    # in another order (a few voxels); later iterations spread those ulps.
+    assert np.mean(snaps[1] == ck[0]) > 0.9999
+    assert np.allclose([r.l2_norm_pre_normalize for r in res.trace.iterations], norms, rtol=1e-9)
 
 
 def test_run_is_normalize_of_step():
