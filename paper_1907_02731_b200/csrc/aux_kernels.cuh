@@ -204,6 +204,9 @@ __global__ void k_finalize_total(const double* frame_sum, float* frame_max, int 
             n.mode = mode_next;
             n.lambda = lambda;
             n.theta = threshold_frac * static_cast<double>(n.max_unit);
+            n.inv_f = static_cast<float>(n.inv);
+            n.theta_f = static_cast<float>(n.theta);
+            n.lambda_f = static_cast<float>(n.lambda);
         }
         *st = n;
     }

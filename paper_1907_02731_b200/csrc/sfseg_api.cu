@@ -180,34 +180,74 @@ CUtensorMap make_tmap(const float* base, int frames, int H, int W, int pitch, in
 // Each instantiation covers radii up to (RT, R) by zero-padding the taps:
 // zero taps add +0 to the float sums, which leaves every value unchanged.
 struct FusedVariant {
-    int rt, r, ty;
+    int rt, r, ty, tx;
+    bool fma;
     size_t smem;
     int threads;
     void (*kernel)(FusedArgs);
     int box_w, box_h;
 };
 
-template <int RT, int R, int TY, int QY>
+template <int RT, int R, int TY, int TX, bool FMA>
 FusedVariant variant() {
-    using G = sfk::FusedGeom<RT, R, 1, TY, 64, QY, 2>;
+    constexpr int QY = 4, ST = 2;
+    using G = sfk::FusedGeom<RT, R, 1, TY, TX, QY, ST>;
     FusedVariant v;
     v.rt = RT;
     v.r = R;
     v.ty = TY;
+    v.tx = TX;
+    v.fma = FMA;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.kernel = sfk::fused_step_exact<RT, R, 1, TY, QY, 2>;
+    v.kernel = sfk::fused_step<RT, R, 1, TY, TX, QY, ST, FMA>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
 }
 
+#define SFK_VARIANTS(FMA_)                                                                \
+    variant<1, 2, 48, 32, FMA_>(), variant<1, 3, 48, 32, FMA_>(),                        \
+        variant<2, 4, 48, 32, FMA_>(), variant<2, 5, 48, 32, FMA_>()
+
 const std::vector<FusedVariant>& variants() {
-    static const std::vector<FusedVariant> v = {
-        variant<1, 2, 32, 8>(), variant<1, 3, 32, 8>(), variant<2, 4, 32, 8>(),
-        variant<2, 5, 32, 8>(),
-    };
+    static const std::vector<FusedVariant> v = {SFK_VARIANTS(false), SFK_VARIANTS(true)};
     return v;
+}
+
+// Host scheduler for the persistent stencil grid: G CTAs, ntiles tiles of
+// Tout output frames. Round 1 gives every CTA floor(ntiles/G) whole tiles
+// (CTA b: tiles b, b+G, ...), so at any time the CTAs sweep neighbouring
+// tiles at the same frame and the halo rows each tile shares with its
+// neighbours are served from L2. The R = ntiles mod G remaining tiles are cut
+// into c = floor(G/R) time chunks; CTA b takes tile (b mod R) chunk (b div R).
+struct Schedule {
+    std::vector<int4> seg;
+    std::vector<int> off;
+};
+
+Schedule build_schedule(int ntiles, int tout, int G) {
+    Schedule s;
+    std::vector<std::vector<int4>> per(G);
+    const int k1 = ntiles / G, rem = ntiles % G;
+    for (int b = 0; b < G; ++b)
+        for (int j = 0; j < k1; ++j) per[b].push_back(make_int4(j * G + b, 0, tout, 0));
+    if (rem > 0) {
+        int c = std::max(1, std::min(G / rem, tout));
+        const int L = (tout + c - 1) / c;
+        c = (tout + L - 1) / L;
+        for (int b = 0; b < rem * c && b < G; ++b) {
+            const int r = b % rem, k = b / rem;
+            const int t0 = k * L, t1 = std::min(tout, (k + 1) * L);
+            if (t0 < t1) per[b].push_back(make_int4(k1 * G + r, t0, t1, 0));
+        }
+    }
+    s.off.push_back(0);
+    for (int b = 0; b < G; ++b) {
+        for (const auto& e : per[b]) s.seg.push_back(e);
+        s.off.push_back(static_cast<int>(s.seg.size()));
+    }
+    return s;
 }
 
 bool env_flag(const char* name) {
@@ -215,13 +255,13 @@ bool env_flag(const char* name) {
     return v && *v && *v != '0';
 }
 
-const FusedVariant* pick_variant(int rt, int ry, int rx) {
+const FusedVariant* pick_variant(int rt, int ry, int rx, bool fma) {
     static const bool force_generic = env_flag("SFSEG_FORCE_GENERIC");
     if (force_generic) return nullptr;
     const int r = std::max(ry, rx);
     const FusedVariant* best = nullptr;
     for (const auto& v : variants())
-        if (v.rt >= rt && v.r >= r) {
+        if (v.fma == fma && v.rt >= rt && v.r >= r) {
             const long cost = (2L * v.rt + 1) * (2L * v.r + 1);
             if (!best || cost < (2L * best->rt + 1) * (2L * best->r + 1)) best = &v;
         }
@@ -265,6 +305,10 @@ struct sfseg_ctx {
     float* bminmax = nullptr;
     double* acc3 = nullptr;
     unsigned long long* cnt2 = nullptr;
+    // persistent-grid schedule (device copy, keyed by ntiles/Tout/G)
+    int4* sched_seg = nullptr;
+    int* sched_off = nullptr;
+    long long sched_key = -1;
     // generic-path temporaries (allocated lazily)
     std::vector<float*> tmp;
     // timing
@@ -425,6 +469,27 @@ void ensure_guard(sfseg_ctx* c, bool guard) {
     c->guard_applied = true;
 }
 
+void upload_schedule(sfseg_ctx* c, int ntiles, int tout, int G) {
+    const long long key = (static_cast<long long>(ntiles) << 40) ^
+                          (static_cast<long long>(tout) << 16) ^ G;
+    if (key == c->sched_key) return;
+    const Schedule s = build_schedule(ntiles, tout, G);
+    if (c->sched_seg) cudaFree(c->sched_seg);
+    if (c->sched_off) cudaFree(c->sched_off);
+    c->sched_seg = nullptr;
+    c->sched_off = nullptr;
+    ck(cudaMalloc(&c->sched_seg, std::max<size_t>(1, s.seg.size()) * sizeof(int4)), "malloc");
+    ck(cudaMalloc(&c->sched_off, s.off.size() * sizeof(int)), "malloc");
+    ck(cudaMemcpyAsync(c->sched_seg, s.seg.data(), s.seg.size() * sizeof(int4),
+                       cudaMemcpyHostToDevice, c->stream),
+       "schedule");
+    ck(cudaMemcpyAsync(c->sched_off, s.off.data(), s.off.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, c->stream),
+       "schedule");
+    ck(cudaStreamSynchronize(c->stream), "schedule");
+    c->sched_key = key;
+}
+
 void fill_taps(FusedArgs& a, const HostKernel& k, const FusedVariant& v) {
     std::memset(a.taps_x, 0, sizeof a.taps_x);
     std::memset(a.taps_y, 0, sizeof a.taps_y);
@@ -444,9 +509,9 @@ float* tmp_vol(sfseg_ctx* c, size_t i) {
 // multi-pass path; emits canonical partials + frame max into c->part /
 // c->frame_max for the whole volume.
 void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
-                 const IterState* st, float* out, const std::vector<float*>& Fch) {
+                 const IterState* st, float* out, const std::vector<float*>& Fch, bool fma) {
     const float inv_alpha = static_cast<float>(1.0 / alpha);
-    const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx);
+    const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx, fma);
     g_conv_count.fetch_add(3ull * Fch.size(), std::memory_order_relaxed);
     if (v) {
         FusedArgs a;
@@ -460,6 +525,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         a.st = st;
         fill_taps(a, k, *v);
         a.inv_alpha = inv_alpha;
+        a.one = 1.0f;
+        a.zero = 0.0f;
         a.T = c->T;
         a.H = c->H;
         a.W = c->W;
@@ -468,13 +535,15 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         a.out_t0 = 0;
         a.out_t1 = c->T;
         a.out_buf_t0 = 0;
-        a.tiles_x = (c->W + 63) / 64;
+        a.tiles_x = (c->W + v->tx - 1) / v->tx;
         a.tiles_y = (c->H + v->ty - 1) / v->ty;
         a.nbands = c->nbands();
         a.nhalves = c->nhalves();
-        const long long units = static_cast<long long>(a.tiles_x) * a.tiles_y * c->T;
-        const long long grid = std::min<long long>(c->num_sms, units);
-        a.units_per_cta = (units + grid - 1) / grid;
+        const int ntiles = a.tiles_x * a.tiles_y;
+        const int grid_n = c->num_sms;
+        upload_schedule(c, ntiles, c->T, grid_n);
+        a.sched = c->sched_seg;
+        a.sched_off = c->sched_off;
         static bool attr_set[64] = {};
         const int vidx = static_cast<int>(v - variants().data());
         if (!attr_set[vidx]) {
@@ -483,7 +552,6 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                "cudaFuncSetAttribute");
             attr_set[vidx] = true;
         }
-        const int grid_n = static_cast<int>((units + a.units_per_cta - 1) / a.units_per_cta);
         for (size_t g = 0; g < Fch.size(); ++g) {
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
             a.f[0] = Fch[g];
@@ -610,7 +678,7 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
     for (int it = first; it <= last; ++it) {
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
-        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->Fw);
+        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->Fw, p->arith == SFSEG_ARITH_FAST);
         const int mode_next = it >= p->binarize_start ? 2 : 1;
         finalize(c, c->st, c->norms, it - first, mode_next, lambda_for(p, it), p->threshold_frac);
         c->cur = dst;
@@ -811,6 +879,8 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         cudaFree(c->acc3);
         cudaFree(c->cnt2);
         if (c->norms) cudaFree(c->norms);
+        if (c->sched_seg) cudaFree(c->sched_seg);
+        if (c->sched_off) cudaFree(c->sched_off);
         for (auto e : c->ev) cudaEventDestroy(e);
         cudaStreamDestroy(c->stream);
         delete c;
@@ -956,7 +1026,7 @@ int sfseg_step(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
         s.mode = 0;
         set_state(c, c->st_aux, s);
         ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
-        launch_step(c, k, p->alpha, xin, c->st_aux, c->y[0], c->F);
+        launch_step(c, k, p->alpha, xin, c->st_aux, c->y[0], c->F, p->arith == SFSEG_ARITH_FAST);
         download(c, out, c->y[0], mem);
         ck(cudaStreamSynchronize(c->stream), "sfseg_step");
         c->sp_p = NAN;  // S is scratch now

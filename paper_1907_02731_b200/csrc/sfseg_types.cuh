@@ -21,6 +21,7 @@ struct IterState {
     int32_t degenerate;  // sticky: some ||y_k|| == 0      (engine.cpp:174-175)
     float max_raw;     // max(0, max y_k)
     float max_unit;    // max(0, max x_unit)
+    float inv_f, theta_f, lambda_f;  // float copies for the FAST arithmetic
 };
 
 // Arguments of one fused stencil launch (one channel group of one step).
@@ -38,12 +39,14 @@ struct FusedArgs {
     float taps_y[kMaxTapsXY];
     float taps_t[kMaxTapsT];
     float inv_alpha;
+    float one, zero;  // 1.0f / 0.0f at run time (keeps ptxas from contracting EXACT FFMA2 pairs)
     int T, H, W, pitch;
     int buf_t0;      // global frame of input buffer frame 0
     int out_t0, out_t1;  // global output frames [out_t0, out_t1)
     int out_buf_t0;  // global frame of output buffer frame 0
     int tiles_x, tiles_y;
-    long long units_per_cta;
+    const int4* sched;   // segments (tile, ta, tb, 0), ta/tb relative to out_t0
+    const int* sched_off;  // CTA b walks sched[sched_off[b] .. sched_off[b+1])
     int first_group, last_group;
     int nbands, nhalves;
 };

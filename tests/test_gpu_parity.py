@@ -130,10 +130,11 @@ def _problem(idx, frames=None, k=0):
     return prob, fs, gt
 
 
+@pytest.mark.parametrize("arith", ["exact", "fast"])
 @pytest.mark.parametrize("binarize", [False, True])
-def test_run_c0_matches_reference(binarize):
+def test_run_c0_matches_reference(binarize, arith):
     prob, fs, _ = _problem(0)
-    cfg = prob.cfg
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith})
     if binarize:
         cfg = E.SfsegConfig(**{**cfg.__dict__, "binarize_start": 3})
     cks = [1, 5, 10, 15, 20]
@@ -145,7 +146,27 @@ def test_run_c0_matches_reference(binarize):
     _gate(res.soft, soft, "final")
     _mask_gate(res.mask, mask, soft, cfg.final_threshold)
     got_norms = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
-    assert np.allclose(got_norms, norms, rtol=1e-10)
+    assert np.allclose(got_norms, norms, rtol=1e-10 if arith == "exact" else 1e-5)
+
+
+@pytest.mark.parametrize("shape,alpha,p,radii,sigmas", STEP_CASES)
+def test_step_fast_within_tolerance(shape, alpha, p, radii, sigmas):
+    S, F = _features(shape, 11)
+    x = random_volume(shape, 99)
+    cfg = _cfg(radii, sigmas, alpha, p, arith="fast")
+    got = E.sfseg_step_channel(x, S, F[0], cfg).astype(np.float64)
+    want = Oracle().step(x, S, F, cfg).astype(np.float64)
+    # FMA vs separately rounded products: a few ulps of the step's scale
+    assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
+
+
+def test_run_c1_cropped_fast_matches_reference():
+    prob, fs, _ = _problem(1, frames=12)
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": "fast"})
+    res = E.run(fs, cfg)
+    soft, mask, norms, _ = Oracle().run(fs.unary, fs.pairwise, cfg)
+    _gate(res.soft, soft, "c1[T=12] fast")
+    _mask_gate(res.mask, mask, soft, cfg.final_threshold)
 
 
 def test_run_c1_cropped_matches_reference():
