@@ -67,6 +67,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// plain arrive (release semantics for this thread's prior shared-memory writes)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier among `n` threads (a subset of the CTA's warps)
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// warpgroup register reallocation (sm_90a+): producers give registers back,
+// consumers (which hold the register rings) take them
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -74,9 +95,9 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
 // ---------------------------------------------------------------------------
 // Canonical sum-of-squares reduction (deterministic, independent of tiling,
 // launch geometry and GPU count):
-//   block  = 8 consecutive rows (y0 % 8 == 0) x 32 consecutive columns
+//   block  = 4 consecutive rows (y0 % 4 == 0) x 32 consecutive columns
 //            (x0 % 32 == 0) of one frame;
-//   column = sequential fp64 sum of x^2 over the 8 rows, top to bottom;
+//   column = sequential fp64 sum of x^2 over the 4 rows, top to bottom;
 //   block  = xor-butterfly (16, 8, 4, 2, 1) over the 32 column sums;
 //   frame  = finalize_frames kernel (fixed order over blocks);
 //   total  = finalize_total kernel (fixed order over frames).

@@ -1,0 +1,474 @@
+// fused_ws.cuh — warp-specialised SFSeg power-iteration step for sm_100a.
+//
+// One kernel per iteration does what the reference spends three
+// convolve_separable calls per channel on (conv3d.cpp:80-185), plus the
+// products (engine.cpp:92-100), recombination and channel sum
+// (engine.cpp:107-120, 157-162) and the sum-of-squares / max scans of
+// normalize_l2 / project_binary (engine.cpp:168-205). The previous
+// iteration's normalisation and sigmoid are applied on load.
+//
+// Roles inside a CTA (NWA + 8 warps, one CTA per SM, persistent over the host
+// schedule of (tile, frame-range) segments; a tile is 64 x 32 points):
+//   A  = the first NWA warps: thread 0 issues the TMA loads of the
+//        (64+2R) x BW halo boxes of y_k, S^p, F_c; all A warps form the
+//        product fields (u = S^p x scalar; (F_c u, F_c^2 u) interleaved
+//        pairs) and run the x-pass into a double-buffered shared tile.
+//   B  = the last 8 warps: each thread owns 4 rows x 2 columns;
+//        it runs the y-pass of those 8 points into a register ring holding
+//        the last 2RT+1 y-filtered planes, the t-pass out of the ring, the
+//        recombination, the store, and the canonical reductions.
+// A and B meet only at two mbarrier pairs per x-pass buffer (full/empty),
+// so the x-pass of plane p+1 overlaps the y/t/epilogue of plane p; A gives
+// registers to B with setmaxnreg (B holds 120 ring registers).
+//
+// Packed arithmetic: two values that take the same tap (two columns of u, or
+// F_c u and F_c^2 u of one column) run as one FFMA2. EXACT keeps the
+// reference's rounding (product, then sum: two FFMA2 with runtime one/zero);
+// FAST fuses them.
+#pragma once
+
+#include <type_traits>
+
+#include "device_common.cuh"
+#include "fused_step.cuh"  // PlaneStream, Arith, canonical_tree32, SFK_RING_SWITCH
+#include "sfseg_types.cuh"
+
+namespace sfk {
+
+template <int RT, int R, int CG, int STAGES, int NWA = 8>
+struct WsGeom {
+    static constexpr int TY = 64, TX = 32;
+    static constexpr int NA = 32 * NWA, NB = 256, NT = NA + NB;
+    // setmaxnreg budgets: the CTA pool is what the launch granted
+    // (65536 / NT rounded down to 8 per thread); asking for more deadlocks
+    static constexpr int RPOOL = (65536 / NT) / 8 * 8;
+    static constexpr int RA = NWA == 4 ? 80 : 56;
+    static constexpr int RB = ((NT * RPOOL - NA * RA) / NB) / 8 * 8;
+    static constexpr int K = 2 * RT + 1;
+    static constexpr int NIN = 2 + CG;
+    static constexpr int BH = TY + 2 * R;
+    static constexpr int RX4 = (R + 3) / 4 * 4;
+    static constexpr int XOFF = RX4 - R;
+    static constexpr int BW = TX + 2 * RX4;
+    static constexpr int BW4 = BW / 4;
+    static constexpr int FB = (BH * BW + 31) / 32 * 32;
+    static constexpr int BWU = BW + 4, BWP = 2 * BW + 4;  // odd float4 row strides
+    static constexpr int PBU = (BH * BWU + 31) / 32 * 32;
+    static constexpr int PBP = (BH * BWP + 31) / 32 * 32;
+    static constexpr int TXU = TX + 4, TXQ = 2 * TX + 4;
+    static constexpr int XBU = (BH * TXU + 31) / 32 * 32;
+    static constexpr int XBP = (BH * TXQ + 31) / 32 * 32;
+    static constexpr int XBUF = XBU + CG * XBP;  // one x-pass buffer
+    static constexpr int SPU = 8, SPP = 8;
+    static constexpr int NSU = TX / SPU, NSP = TX / SPP;
+    static constexpr int XU_ITEMS = NSU * BH, XITEMS = XU_ITEMS + CG * NSP * BH;
+    static constexpr int NINU = SPU + 2 * R, NINP = SPP + 2 * R;
+    static constexpr int NBANDS = TY / 4;
+    static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
+    static constexpr size_t PROD_FLOATS = size_t(PBU) + size_t(CG) * PBP;
+    static constexpr size_t XB_FLOATS = 2 * size_t(XBUF);
+    static constexpr size_t RED_FLOATS = 2 * (2 * NBANDS * 32) + 2 * 16;  // doubles + warp max
+    static constexpr size_t SMEM_BYTES =
+        (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + RED_FLOATS) * sizeof(float) + 128;
+    static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
+    static_assert(NA * RA + NB * RB <= NT * RPOOL, "register pool of the CTA");
+    static_assert(RB <= 248, "setmaxnreg range");
+    static_assert(BW <= 256 && BH <= 256, "TMA box limit");
+    static_assert((BWU / 4) % 2 == 1 && (BWP / 4) % 2 == 1, "conflict-free product rows");
+    static_assert((TXU / 4) % 2 == 1 && (TXQ / 4) % 2 == 1, "conflict-free x-pass rows");
+    static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
+};
+
+template <int RT, int R, int CG, int STAGES, bool FMA, int NWA = 8>
+__global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_constant__ FusedArgs a) {
+    using G = WsGeom<RT, R, CG, STAGES, NWA>;
+    using A = Arith<FMA>;
+    constexpr int TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K;
+    constexpr int NIN = G::NIN, BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4;
+    constexpr int BWU = G::BWU, BWP = G::BWP, PBU = G::PBU, PBP = G::PBP;
+    constexpr int TXU = G::TXU, TXQ = G::TXQ, XBU = G::XBU, XBP = G::XBP, XBUF = G::XBUF;
+
+    extern __shared__ __align__(128) float smem[];
+    float* raw = smem;                      // [STAGES][NIN][FB]   TMA boxes
+    float* produ = raw + G::RAW_FLOATS;     // [BH][BWU]           u
+    float* prodp = produ + PBU;             // [CG][BH][BWP]       (F u, F^2 u)
+    float* xb = prodp + CG * PBP;           // [2][XBUF]           x-pass output
+    double* red = reinterpret_cast<double*>(xb + G::XB_FLOATS);  // [2][NBANDS][32]
+    float* redmax = reinterpret_cast<float*>(red + 2 * G::NBANDS * 32);  // [2][8]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(redmax + 2 * 16);
+    uint64_t* raw_full = mbar;             // [STAGES]  TMA -> A
+    uint64_t* xb_full = mbar + STAGES;     // [2]       A -> B (count NA)
+    uint64_t* xb_empty = mbar + STAGES + 2;  // [2]     B -> A (count NB)
+
+    __shared__ IterState st;
+    __shared__ PlaneStream prodq;
+    __shared__ int prod_count;
+
+    const int tid = threadIdx.x;
+    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
+    if (s0 >= s1) return;
+
+    if (tid == 0) {
+        st = *a.st;
+        for (int s = 0; s < STAGES; ++s) mbar_init(&raw_full[s], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&xb_full[b], NA);
+            mbar_init(&xb_empty[b], NB);
+        }
+        fence_barrier_init();
+        prefetch_tensormap(&a.tm_x);
+        prefetch_tensormap(&a.tm_sp);
+        for (int c = 0; c < CG; ++c) prefetch_tensormap(&a.tm_f[c]);
+    }
+    __syncthreads();
+
+    const float2 one2 = make_float2(a.one, a.one), zero2 = make_float2(a.zero, a.zero);
+
+    if (tid < NA) {
+        // =====================================================================
+        // A: TMA producer + products + x-pass
+        // =====================================================================
+        setmaxnreg_dec<G::RA>();
+        auto issue_next = [&]() {
+            while (!prodq.done) {
+                const int tg = a.out_t0 + prodq.p;
+                if (tg >= 0 && tg < a.T) break;
+                prodq.next();
+            }
+            if (prodq.done) return;
+            const int tg = a.out_t0 + prodq.p;
+            const int s = prod_count % STAGES;
+            float* dst = raw + static_cast<size_t>(s) * NIN * FB;
+            uint64_t* bar = &raw_full[s];
+            mbar_arrive_expect_tx(bar, NIN * BH * BW * sizeof(float));
+            const int bx = prodq.tile_x * TX - G::RX4, by = prodq.tile_y * TY - R,
+                      bt = tg - a.buf_t0;
+            tma_load_3d(dst, &a.tm_x, bar, bx, by, bt);
+            tma_load_3d(dst + FB, &a.tm_sp, bar, bx, by, bt);
+#pragma unroll
+            for (int c = 0; c < CG; ++c)
+                tma_load_3d(dst + (2 + c) * FB, &a.tm_f[c], bar, bx, by, bt);
+            ++prod_count;
+            prodq.next();
+        };
+        if (tid == 0) {
+            prodq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            prod_count = 0;
+            for (int s = 0; s < STAGES; ++s) issue_next();
+        }
+        const bool sigm = st.mode == 2;
+        const double inv = st.mode == 0 ? 1.0 : st.inv;  // float(double(y)*1.0) == y
+        const float inv_f = st.mode == 0 ? 1.0f : st.inv_f;
+
+        PlaneStream q;
+        q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+        int cnt = 0;  // in-volume planes handled
+        for (; !q.done; q.next()) {
+            const int tg = a.out_t0 + q.p;
+            if (tg < 0 || tg >= a.T) continue;  // planes outside the volume: B zero-fills
+            const int s = cnt % STAGES;
+            mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
+            const float* rs = raw + static_cast<size_t>(s) * NIN * FB;
+            // products over the halo box (engine.cpp:92-100), 4 points per item
+            for (int i = tid; i < BH * BW4; i += NA) {
+                const int r = i / BW4, c4 = i - r * BW4;
+                const float4 yv = reinterpret_cast<const float4*>(rs)[i];
+                const float4 sv = reinterpret_cast<const float4*>(rs + FB)[i];
+                float4 xv;
+                if (sigm) {
+                    xv.x = A::load_sigmoid(yv.x, st);
+                    xv.y = A::load_sigmoid(yv.y, st);
+                    xv.z = A::load_sigmoid(yv.z, st);
+                    xv.w = A::load_sigmoid(yv.w, st);
+                } else {
+                    xv.x = A::load_norm(yv.x, inv, inv_f);
+                    xv.y = A::load_norm(yv.y, inv, inv_f);
+                    xv.z = A::load_norm(yv.z, inv, inv_f);
+                    xv.w = A::load_norm(yv.w, inv, inv_f);
+                }
+                float4 u;
+                u.x = A::mul(sv.x, xv.x);
+                u.y = A::mul(sv.y, xv.y);
+                u.z = A::mul(sv.z, xv.z);
+                u.w = A::mul(sv.w, xv.w);
+                *reinterpret_cast<float4*>(produ + r * BWU + 4 * c4) = u;
+#pragma unroll
+                for (int cg = 0; cg < CG; ++cg) {
+                    const float4 fv = reinterpret_cast<const float4*>(rs + (2 + cg) * FB)[i];
+                    float4 p0, p1;  // (F S^p X, (F F) S^p X) per point
+                    p0.x = A::mul(fv.x, u.x);
+                    p0.y = A::mul(A::mul(fv.x, fv.x), u.x);
+                    p0.z = A::mul(fv.y, u.y);
+                    p0.w = A::mul(A::mul(fv.y, fv.y), u.y);
+                    p1.x = A::mul(fv.z, u.z);
+                    p1.y = A::mul(A::mul(fv.z, fv.z), u.z);
+                    p1.z = A::mul(fv.w, u.w);
+                    p1.w = A::mul(A::mul(fv.w, fv.w), u.w);
+                    float4* pp = reinterpret_cast<float4*>(prodp + cg * PBP + r * BWP + 8 * c4);
+                    pp[0] = p0;
+                    pp[1] = p1;
+                }
+            }
+            named_bar_sync(1, NA);  // products ready; raw stage s fully read
+            if (tid == 0) {
+                fence_proxy_async();  // generic reads of stage s before the TMA overwrite
+                issue_next();
+            }
+            // x-pass (conv3d.cpp:88-101) into the free x buffer
+            const int b = cnt & 1;
+            mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
+            float* xbu = xb + b * XBUF;
+            float* xbp = xbu + XBU;
+            for (int it = tid; it < G::XITEMS; it += NA) {
+                if (it < G::XU_ITEMS) {
+                    const int r = it % BH, sidx = it / BH;
+                    const float4* src = reinterpret_cast<const float4*>(produ + r * BWU + sidx * G::SPU);
+                    float o[G::SPU];
+                    float4 q4;
+#pragma unroll
+                    for (int m4 = 0; m4 < (G::XOFF + G::NINU + 3) / 4 * 4; ++m4) {
+                        if (m4 % 4 == 0) q4 = src[m4 / 4];
+                        const int m = m4 - G::XOFF;
+                        if (m < 0 || m >= G::NINU) continue;
+                        const float vin = (m4 % 4 == 0) ? q4.x : (m4 % 4 == 1) ? q4.y
+                                        : (m4 % 4 == 2) ? q4.z : q4.w;
+#pragma unroll
+                        for (int j = 0; j < G::SPU; ++j) {
+                            const int d = m - j;
+                            if (d < 0 || d > 2 * R) continue;
+                            o[j] = d == 0 ? A::mul(a.taps_x[0], vin) : A::mac(o[j], a.taps_x[d], vin);
+                        }
+                    }
+                    float4* dst = reinterpret_cast<float4*>(xbu + r * TXU + sidx * G::SPU);
+#pragma unroll
+                    for (int v = 0; v < G::SPU / 4; ++v)
+                        dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+                } else {
+                    const int jt = it - G::XU_ITEMS;
+                    const int r = jt % BH, sidx = (jt / BH) % G::NSP, c = jt / (BH * G::NSP);
+                    const float4* src = reinterpret_cast<const float4*>(
+                        prodp + c * PBP + r * BWP + 2 * sidx * G::SPP);
+                    float2 o[G::SPP];
+                    float4 q4;
+#pragma unroll
+                    for (int m2 = 0; m2 < (G::XOFF + G::NINP + 1) / 2 * 2; ++m2) {
+                        if (m2 % 2 == 0) q4 = src[m2 / 2];
+                        const int m = m2 - G::XOFF;
+                        if (m < 0 || m >= G::NINP) continue;
+                        const float2 vin = (m2 % 2 == 0) ? make_float2(q4.x, q4.y)
+                                                         : make_float2(q4.z, q4.w);
+#pragma unroll
+                        for (int j = 0; j < G::SPP; ++j) {
+                            const int d = m - j;
+                            if (d < 0 || d > 2 * R) continue;
+                            o[j] = d == 0 ? A::mul2(a.taps_x[0], vin, zero2)
+                                          : A::mac2(o[j], a.taps_x[d], vin, one2, zero2);
+                        }
+                    }
+                    float4* dst = reinterpret_cast<float4*>(xbp + c * XBP + r * TXQ + 2 * sidx * G::SPP);
+#pragma unroll
+                    for (int v = 0; v < G::SPP / 2; ++v)
+                        dst[v] = make_float4(o[2 * v].x, o[2 * v].y, o[2 * v + 1].x, o[2 * v + 1].y);
+                }
+            }
+            mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
+            named_bar_sync(1, NA);     // every A thread is done with the products
+            ++cnt;
+        }
+    } else {
+        // =====================================================================
+        // B: y-pass ring, t-pass, recombination, store, reductions
+        // =====================================================================
+        setmaxnreg_inc<G::RB>();
+        const int bt = tid - NA;
+        const int band = bt >> 4;         // rows 4*band .. 4*band+3 of the tile
+        const int cp = bt & 15;           // columns 2cp, 2cp+1
+        const int bwarp = bt >> 5;
+        const float inv_alpha = a.inv_alpha;
+
+        float2 ringu[4][K];          // (col 2cp, col 2cp+1) of u
+        float2 ringp[CG][4][2][K];   // (F u, F^2 u) per column
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                ringu[r][k] = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int c = 0; c < CG; ++c) {
+                    ringp[c][r][0][k] = make_float2(0.0f, 0.0f);
+                    ringp[c][r][1][k] = make_float2(0.0f, 0.0f);
+                }
+            }
+
+        PlaneStream q;
+        q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+        int cnt = 0, slot = 0, outc = 0;
+        for (; !q.done; q.next()) {
+            const int tg = a.out_t0 + q.p;
+            const bool valid = tg >= 0 && tg < a.T;
+            const int out_p = q.p - RT;
+            const bool emit = out_p >= q.ta;
+            const int to = a.out_t0 + out_p;
+            const int y0 = q.tile_y * TY + band * 4;
+            const int x0 = q.tile_x * TX + 2 * cp;
+            const int rows = x0 < a.W ? min(4, a.H - y0) : 0;
+            // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending)
+            float2 yu[4];
+            float2 yp[CG][4][2];
+            if (valid) {
+                const int b = cnt & 1;
+                mbar_wait(&xb_full[b], (cnt >> 1) & 1);
+                const float* xbu = xb + b * XBUF;
+                const float* xbp = xbu + XBU;
+                const float2* su = reinterpret_cast<const float2*>(xbu + (band * 4) * TXU) + cp;
+#pragma unroll
+                for (int j = 0; j < 4 + 2 * R; ++j) {
+                    const float2 vin = su[j * (TXU / 2)];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int d = j - r;
+                        if (d < 0 || d > 2 * R) continue;
+                        yu[r] = d == 0 ? A::mul2(a.taps_y[0], vin, zero2)
+                                       : A::mac2(yu[r], a.taps_y[d], vin, one2, zero2);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < CG; ++c) {
+                    const float4* sp4 =
+                        reinterpret_cast<const float4*>(xbp + c * XBP + (band * 4) * TXQ) + cp;
+#pragma unroll
+                    for (int j = 0; j < 4 + 2 * R; ++j) {
+                        const float4 v4 = sp4[j * (TXQ / 4)];
+                        const float2 v0 = make_float2(v4.x, v4.y), v1 = make_float2(v4.z, v4.w);
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int d = j - r;
+                            if (d < 0 || d > 2 * R) continue;
+                            if (d == 0) {
+                                yp[c][r][0] = A::mul2(a.taps_y[0], v0, zero2);
+                                yp[c][r][1] = A::mul2(a.taps_y[0], v1, zero2);
+                            } else {
+                                yp[c][r][0] = A::mac2(yp[c][r][0], a.taps_y[d], v0, one2, zero2);
+                                yp[c][r][1] = A::mac2(yp[c][r][1], a.taps_y[d], v1, one2, zero2);
+                            }
+                        }
+                    }
+                }
+                mbar_arrive(&xb_empty[b]);
+                ++cnt;
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    yu[r] = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int c = 0; c < CG; ++c) yp[c][r][0] = yp[c][r][1] = make_float2(0.0f, 0.0f);
+                }
+            }
+            // prefetch S^p and F_c of the output plane (L2-resident: loaded by
+            // TMA RT planes ago); latency hides behind the t-pass of the other warps
+            float2 spv[4], fv[CG][4];
+            if (emit) {
+                const size_t base =
+                    (static_cast<size_t>(to - a.buf_t0) * a.H + y0) * a.pitch + x0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.sp + base + r * a.pitch))
+                                      : make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int c = 0; c < CG; ++c)
+                        fv[c][r] = r < rows
+                                       ? __ldg(reinterpret_cast<const float2*>(a.f[c] + base + r * a.pitch))
+                                       : make_float2(0.0f, 0.0f);
+                }
+            }
+            // t-pass (conv3d.cpp:147-165) out of the ring, row by row, each row
+            // recombined and stored at once (keeps few values live); planes
+            // oldest..newest take taps_t[0..2RT]; a switch on the slot keeps
+            // the ring indices static
+            const bool first = a.first_group;
+            float* orow = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + y0) * a.pitch + x0;
+            double cs0 = 0.0, cs1 = 0.0;
+            float cmax = 0.0f;
+            auto t_step = [&](auto slot_c) {
+                constexpr int S_ = decltype(slot_c)::value;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    ringu[r][S_] = yu[r];
+                    float2 zu = A::mul2(a.taps_t[0], ringu[r][(S_ + 1) % K], zero2);
+#pragma unroll
+                    for (int d = 1; d < K; ++d)
+                        zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % K], one2, zero2);
+                    float2 zp[CG][2];
+#pragma unroll
+                    for (int c = 0; c < CG; ++c)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            ringp[c][r][j][S_] = yp[c][r][j];
+                            float2 acp = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % K], zero2);
+#pragma unroll
+                            for (int d = 1; d < K; ++d)
+                                acp = A::mac2(acp, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % K],
+                                              one2, zero2);
+                            zp[c][j] = acp;
+                        }
+                    if (!emit) continue;
+                    // recombination + channel sum (engine.cpp:113-119, 157-162), store
+                    float2 prev = make_float2(0.0f, 0.0f);
+                    if (!first && r < rows) prev = *reinterpret_cast<const float2*>(orow + r * a.pitch);
+                    float v[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float Au = j ? zu.y : zu.x;
+                        const float sp_ = j ? spv[r].y : spv[r].x;
+                        float acc = 0.0f;
+#pragma unroll
+                        for (int c = 0; c < CG; ++c) {
+                            const float f_ = j ? fv[c][r].y : fv[c][r].x;
+                            const float term =
+                                A::recombine(sp_, f_, inv_alpha, Au, zp[c][j].y, zp[c][j].x);
+                            acc = c > 0 ? xadd(acc, term)
+                                        : (first ? term : xadd(j ? prev.y : prev.x, term));
+                        }
+                        v[j] = acc;
+                    }
+                    if (r < rows) *reinterpret_cast<float2*>(orow + r * a.pitch) = make_float2(v[0], v[1]);
+                    // only points inside the volume enter the reductions
+                    const float v0 = r < rows ? v[0] : 0.0f;
+                    const float v1 = (r < rows && x0 + 1 < a.W) ? v[1] : 0.0f;
+                    cs0 += static_cast<double>(v0) * static_cast<double>(v0);
+                    cs1 += static_cast<double>(v1) * static_cast<double>(v1);
+                    cmax = fmaxf(cmax, fmaxf(v0, v1));
+                }
+            };
+            SFK_RING_SWITCH(slot, t_step)
+            slot = (slot + 1 == K) ? 0 : slot + 1;
+            if (!emit) continue;
+            if (a.last_group) {
+                const int buf = outc & 1;
+                double* rb = red + buf * (G::NBANDS * 32);
+                rb[band * 32 + 2 * cp] = cs0;
+                rb[band * 32 + 2 * cp + 1] = cs1;
+                const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                if ((bt & 31) == 0) redmax[buf * 16 + bwarp] = __int_as_float(wm);
+                named_bar_sync(2, NB);
+                if (bwarp == 0) {  // canonical 32-column tree per 4-row band
+                    const int lane = bt & 31;
+                    if (lane < G::NBANDS) {
+                        const double s = canonical_tree32(rb + lane * 32);
+                        const int gband = q.tile_y * G::NBANDS + lane;
+                        if (gband < a.nbands && q.tile_x < a.nhalves)
+                            a.part[(static_cast<size_t>(to) * a.nbands + gband) * a.nhalves +
+                                   q.tile_x] = s;
+                    }
+                    float m = lane < NB / 32 ? redmax[buf * 16 + lane] : 0.0f;
+                    m = butterfly_max32(m);
+                    if (lane == 0) atomic_max_nonneg(a.frame_max + to, m);
+                }
+                ++outc;
+            }
+        }
+    }
+}
+
+}  // namespace sfk

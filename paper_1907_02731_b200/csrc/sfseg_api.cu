@@ -22,6 +22,7 @@
 #include "../../include/sfseg_cuda.h"
 #include "aux_kernels.cuh"
 #include "fused_step.cuh"
+#include "fused_ws.cuh"
 
 namespace {
 
@@ -206,13 +207,41 @@ FusedVariant variant() {
     return v;
 }
 
+template <int RT, int R, bool FMA, int NWA = 8>
+FusedVariant variant_ws() {
+    using G = sfk::WsGeom<RT, R, 1, 2, NWA>;
+    FusedVariant v;
+    v.rt = RT;
+    v.r = R;
+    v.ty = G::TY;
+    v.tx = G::TX;
+    v.fma = FMA;
+    v.smem = G::SMEM_BYTES;
+    v.threads = G::NT;
+    v.kernel = sfk::fused_step_ws<RT, R, 1, 2, FMA, NWA>;
+    v.box_w = G::BW;
+    v.box_h = G::BH;
+    return v;
+}
+
+#define SFK_VARIANTS_WS(FMA_)                                                             \
+    variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \
+        variant_ws<2, 5, FMA_>()
+
 #define SFK_VARIANTS(FMA_)                                                                \
     variant<1, 2, 48, 32, FMA_>(), variant<1, 3, 48, 32, FMA_>(),                        \
         variant<2, 4, 48, 32, FMA_>(), variant<2, 5, 48, 32, FMA_>()
 
+// SFSEG_KERNEL=v4 selects the single-role kernel (fused_step.cuh) for
+// comparison; the default is the warp-specialised one (fused_ws.cuh).
 const std::vector<FusedVariant>& variants() {
-    static const std::vector<FusedVariant> v = {SFK_VARIANTS(false), SFK_VARIANTS(true)};
-    return v;
+    static const bool v4 = [] {
+        const char* e = std::getenv("SFSEG_KERNEL");
+        return e && std::string(e) == "v4";
+    }();
+    static const std::vector<FusedVariant> ws = {SFK_VARIANTS_WS(false), SFK_VARIANTS_WS(true)};
+    static const std::vector<FusedVariant> old = {SFK_VARIANTS(false), SFK_VARIANTS(true)};
+    return v4 ? old : ws;
 }
 
 // Host scheduler for the persistent stencil grid: G CTAs, ntiles tiles of
