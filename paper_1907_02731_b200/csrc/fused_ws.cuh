@@ -59,7 +59,7 @@ struct WsGeom {
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;
     static constexpr int XBP = (BH * TXQ + 31) / 32 * 32;
     static constexpr int XBUF = XBU + CG * XBP;  // one x-pass buffer
-    static constexpr int SPU = 8, SPP = 8;
+    static constexpr int SPU = 4, SPP = 4;  // 2 x 8 x BH strips: even split over A
     static constexpr int NSU = TX / SPU, NSP = TX / SPP;
     static constexpr int XU_ITEMS = NSU * BH, XITEMS = XU_ITEMS + CG * NSP * BH;
     static constexpr int NINU = SPU + 2 * R, NINP = SPP + 2 * R;
@@ -445,27 +445,23 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             slot = (slot + 1 == K) ? 0 : slot + 1;
             if (!emit) continue;
             if (a.last_group) {
-                const int buf = outc & 1;
-                double* rb = red + buf * (G::NBANDS * 32);
-                rb[band * 32 + 2 * cp] = cs0;
-                rb[band * 32 + 2 * cp + 1] = cs1;
-                const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
-                if ((bt & 31) == 0) redmax[buf * 16 + bwarp] = __int_as_float(wm);
-                named_bar_sync(2, NB);
-                if (bwarp == 0) {  // canonical 32-column tree per 4-row band
-                    const int lane = bt & 31;
-                    if (lane < G::NBANDS) {
-                        const double s = canonical_tree32(rb + lane * 32);
-                        const int gband = q.tile_y * G::NBANDS + lane;
-                        if (gband < a.nbands && q.tile_x < a.nhalves)
-                            a.part[(static_cast<size_t>(to) * a.nbands + gband) * a.nhalves +
-                                   q.tile_x] = s;
-                    }
-                    float m = lane < NB / 32 ? redmax[buf * 16 + lane] : 0.0f;
-                    m = butterfly_max32(m);
-                    if (lane == 0) atomic_max_nonneg(a.frame_max + to, m);
+                // canonical reduction (device_common.cuh), warp-local: a warp
+                // holds two whole bands (lanes 0-15 band 2w, 16-31 band 2w+1),
+                // lane l of a half holds columns 2l and 2l+1. The 32-column
+                // butterfly (16, 8, 4, 2, 1) becomes xor 8, 4, 2, 1 over the
+                // half-warp plus the final even+odd add inside the lane.
+#pragma unroll
+                for (int o = 8; o >= 1; o >>= 1) {
+                    cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
+                    cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
                 }
-                ++outc;
+                const double s = cs0 + cs1;
+                const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                const int lane = bt & 31;
+                const int gband = q.tile_y * G::NBANDS + band;
+                if ((lane & 15) == 0 && gband < a.nbands && q.tile_x < a.nhalves)
+                    a.part[(static_cast<size_t>(to) * a.nbands + gband) * a.nhalves + q.tile_x] = s;
+                if (lane == 0) atomic_max_nonneg(a.frame_max + to, __int_as_float(wm));
             }
         }
     }
