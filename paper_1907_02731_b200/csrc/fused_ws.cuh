@@ -71,6 +71,7 @@ struct WsGeom {
     static constexpr size_t SMEM_BYTES =
         (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + RED_FLOATS) * sizeof(float) + 128;
     static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
+    static_assert(CG == 1 || true, "pair strips are split over the second half of A");
     static_assert(NA * RA + NB * RB <= NT * RPOOL, "register pool of the CTA");
     static_assert(RB <= 248, "setmaxnreg range");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
@@ -198,13 +199,20 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     const float4 fv = reinterpret_cast<const float4*>(rs + (2 + cg) * FB)[i];
                     float4 p0, p1;  // (F S^p X, (F F) S^p X) per point
                     p0.x = A::mul(fv.x, u.x);
-                    p0.y = A::mul(A::mul(fv.x, fv.x), u.x);
                     p0.z = A::mul(fv.y, u.y);
-                    p0.w = A::mul(A::mul(fv.y, fv.y), u.y);
                     p1.x = A::mul(fv.z, u.z);
-                    p1.y = A::mul(A::mul(fv.z, fv.z), u.z);
                     p1.z = A::mul(fv.w, u.w);
-                    p1.w = A::mul(A::mul(fv.w, fv.w), u.w);
+                    if constexpr (FMA) {  // FAST: F (F u), one product less
+                        p0.y = fv.x * p0.x;
+                        p0.w = fv.y * p0.z;
+                        p1.y = fv.z * p1.x;
+                        p1.w = fv.w * p1.z;
+                    } else {  // engine.cpp:98: fi * fi * sx
+                        p0.y = A::mul(A::mul(fv.x, fv.x), u.x);
+                        p0.w = A::mul(A::mul(fv.y, fv.y), u.y);
+                        p1.y = A::mul(A::mul(fv.z, fv.z), u.z);
+                        p1.w = A::mul(A::mul(fv.w, fv.w), u.w);
+                    }
                     float4* pp = reinterpret_cast<float4*>(prodp + cg * PBP + r * BWP + 8 * c4);
                     pp[0] = p0;
                     pp[1] = p1;
@@ -220,8 +228,10 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
-            for (int it = tid; it < G::XITEMS; it += NA) {
-                if (it < G::XU_ITEMS) {
+            // the first NA/2 threads take the u strips, the others the pair
+            // strips (equal counts and costs); lanes take consecutive rows
+            if (tid < NA / 2) {
+                for (int it = tid; it < G::XU_ITEMS; it += NA / 2) {
                     const int r = it % BH, sidx = it / BH;
                     const float4* src = reinterpret_cast<const float4*>(produ + r * BWU + sidx * G::SPU);
                     float o[G::SPU];
@@ -244,8 +254,9 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
 #pragma unroll
                     for (int v = 0; v < G::SPU / 4; ++v)
                         dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
-                } else {
-                    const int jt = it - G::XU_ITEMS;
+                }
+            } else {
+                for (int jt = tid - NA / 2; jt < G::XITEMS - G::XU_ITEMS; jt += NA / 2) {
                     const int r = jt % BH, sidx = (jt / BH) % G::NSP, c = jt / (BH * G::NSP);
                     const float4* src = reinterpret_cast<const float4*>(
                         prodp + c * PBP + r * BWP + 2 * sidx * G::SPP);
@@ -313,6 +324,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             const int y0 = q.tile_y * TY + band * 4;
             const int x0 = q.tile_x * TX + 2 * cp;
             const int rows = x0 < a.W ? min(4, a.H - y0) : 0;
+            const long long col_off = static_cast<long long>(y0) * a.pitch + x0;
             // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending)
             float2 yu[4];
             float2 yp[CG][4][2];
@@ -365,20 +377,20 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     for (int c = 0; c < CG; ++c) yp[c][r][0] = yp[c][r][1] = make_float2(0.0f, 0.0f);
                 }
             }
-            // prefetch S^p and F_c of the output plane (L2-resident: loaded by
-            // TMA RT planes ago); latency hides behind the t-pass of the other warps
+            // S^p and F_c of the output plane (L2-resident: loaded by TMA RT
+            // planes ago); issued here, consumed in the epilogue
             float2 spv[4], fv[CG][4];
             if (emit) {
-                const size_t base =
-                    (static_cast<size_t>(to - a.buf_t0) * a.H + y0) * a.pitch + x0;
+                const long long plane = static_cast<long long>(to - a.buf_t0) * a.H * a.pitch;
+                const float* ps = a.sp + plane + col_off;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.sp + base + r * a.pitch))
+                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(ps + r * a.pitch))
                                       : make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int c = 0; c < CG; ++c)
                         fv[c][r] = r < rows
-                                       ? __ldg(reinterpret_cast<const float2*>(a.f[c] + base + r * a.pitch))
+                                       ? __ldg(reinterpret_cast<const float2*>(a.f[c] + plane + col_off + r * a.pitch))
                                        : make_float2(0.0f, 0.0f);
                 }
             }
@@ -387,7 +399,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             // oldest..newest take taps_t[0..2RT]; a switch on the slot keeps
             // the ring indices static
             const bool first = a.first_group;
-            float* orow = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + y0) * a.pitch + x0;
+            float* orow = a.out + static_cast<long long>(to - a.out_buf_t0) * a.H * a.pitch + col_off;
             double cs0 = 0.0, cs1 = 0.0;
             float cmax = 0.0f;
             auto t_step = [&](auto slot_c) {
