@@ -201,6 +201,47 @@ int sfseg_convolve_separable(sfseg_ctx* ctx, uint32_t frames, uint32_t height,
  * channel-step are counted as 3 per channel, as the reference does. */
 uint64_t sfseg_separable_convolution_count(void);
 
+/* ---- time-sharded multi-GPU solve (one process per GPU) ---------------- */
+/*
+ * A rank owns output frames [out_t0, out_t1) of a T-frame problem and keeps a
+ * local buffer of frames [max(0, out_t0 - halo), min(T, out_t1 + halo)) with
+ * halo = the kernel's time radius. Zero padding applies only at the global
+ * ends (frame 0 and T-1), exactly as in conv3d.cpp:149-151. Per iteration the
+ * caller (the NCCL driver in paper_1907_02731_b200/sharding.py):
+ *   1. sfseg_shard_step: fused stencil over the rank's frames + its per-frame
+ *      canonical sums / max (io describes the device buffers to exchange);
+ *   2. sends io.send_lo to rank-1 (its recv_hi) and io.send_hi to rank+1 (its
+ *      recv_lo): the edge frames of the new iterate;
+ *   3. all-gathers io.frame_sum / io.frame_max into global [T] arrays;
+ *   4. sfseg_shard_finalize with the global arrays: every rank derives the
+ *      same norm and projection scalars, summed in frame order, so results
+ *      are bit-identical for any number of ranks.
+ */
+typedef struct sfseg_shard_io {
+    void* send_lo;           /* first `halo` output frames of the new iterate */
+    void* send_hi;           /* last `halo` output frames of the new iterate */
+    void* recv_lo;           /* halo frames below out_t0 (filled by rank-1) */
+    void* recv_hi;           /* halo frames from out_t1 (filled by rank+1) */
+    uint64_t send_lo_bytes, send_hi_bytes, recv_lo_bytes, recv_hi_bytes;
+    double* frame_sum;       /* [out_t1-out_t0] canonical sum of y^2 per frame */
+    float* frame_max;        /* [out_t1-out_t0] max(0, y) per frame */
+    int32_t out_frames;
+    int32_t halo;
+} sfseg_shard_io;
+
+/* unary / pairwise / x0 hold the local buffer frames (dense, as above). */
+int sfseg_shard_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                     int32_t channels, int32_t out_t0, int32_t out_t1, int32_t halo,
+                     const float* unary, const float* const* pairwise, const float* x0,
+                     int32_t mem);
+int sfseg_shard_step(sfseg_ctx* ctx, const sfseg_params* p, int32_t iter, sfseg_shard_io* io);
+/* frame_sum / frame_max: global [frames] arrays (device or host, per mem). */
+int sfseg_shard_finalize(sfseg_ctx* ctx, const sfseg_params* p, int32_t iter,
+                         const double* frame_sum, const float* frame_max, double* norm,
+                         int32_t mem);
+/* Soft iterate / mask of the rank's output frames; frac as threshold_final. */
+int sfseg_shard_download(sfseg_ctx* ctx, double frac, float* soft, uint8_t* mask, int32_t mem);
+
 #ifdef __cplusplus
 }
 #endif

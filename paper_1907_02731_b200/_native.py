@@ -109,6 +109,17 @@ class Timing(C.Structure):
     ]
 
 
+class ShardIO(C.Structure):
+    _fields_ = [
+        ("send_lo", C.c_void_p), ("send_hi", C.c_void_p),
+        ("recv_lo", C.c_void_p), ("recv_hi", C.c_void_p),
+        ("send_lo_bytes", C.c_uint64), ("send_hi_bytes", C.c_uint64),
+        ("recv_lo_bytes", C.c_uint64), ("recv_hi_bytes", C.c_uint64),
+        ("frame_sum", C.c_void_p), ("frame_max", C.c_void_p),
+        ("out_frames", C.c_int32), ("halo", C.c_int32),
+    ]
+
+
 _lib = None
 
 _P = C.c_void_p
@@ -143,6 +154,11 @@ _SIGS = {
     "sfseg_convolve_separable": (C.c_int, [_P, _U32, _U32, _U32, _P, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_double), _P, _I32]),
     "sfseg_separable_convolution_count": (C.c_uint64, []),
+    "sfseg_shard_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32]),
+    "sfseg_shard_step": (C.c_int, [_P, C.POINTER(Params), _I32, C.POINTER(ShardIO)]),
+    "sfseg_shard_finalize": (C.c_int, [_P, C.POINTER(Params), _I32, _P, _P,
+                                       C.POINTER(C.c_double), _I32]),
+    "sfseg_shard_download": (C.c_int, [_P, C.c_double, _P, _P, _I32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

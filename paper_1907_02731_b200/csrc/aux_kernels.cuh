@@ -227,6 +227,18 @@ __global__ void k_transform(Vol y, Vol out, const IterState* stp) {
     }
 }
 
+// max of the projected iterate x = T(y) from the state (T is monotone, so
+// max x = T(max y)); used for the hard mask of a time shard
+__global__ void k_state_max(const IterState* stp, float* out) {
+    const IterState st = *stp;
+    float m = st.max_unit;
+    if (st.mode == 2) {
+        const double z = st.lambda * (static_cast<double>(m) - st.theta);
+        m = static_cast<float>(1.0 / (1.0 + exp(-z)));
+    }
+    *out = m;
+}
+
 // max(0, max v) (engine.cpp:189-190, 208-210)
 __global__ void k_max(Vol v, float* out) {
     float m = 0.0f;

@@ -355,12 +355,12 @@ __global__ void __launch_bounds__(FusedGeom<RT, R, CG, TY, TX, QY, STAGES>::NT, 
             const int band = pend_tile_y * G::NBANDS + band_l;
             const int half = pend_tile_x * G::NHALVES + half_l;
             if (band < a.nbands && half < a.nhalves)
-                a.part[(static_cast<size_t>(pend_to) * a.nbands + band) * a.nhalves + half] = s;
+                a.part[(static_cast<size_t>(pend_to - a.part_t0) * a.nbands + band) * a.nhalves + half] = s;
         }
         if (a.last_group) {
             float m = lane < NT / 32 ? redmax[pend_buf * 32 + lane] : 0.0f;
             m = butterfly_max32(m);
-            if (lane == 0) atomic_max_nonneg(a.frame_max + pend_to, m);
+            if (lane == 0) atomic_max_nonneg(a.frame_max + (pend_to - a.part_t0), m);
         }
     };
 

@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 const int lane = bt & 31;
                 const int gband = q.tile_y * G::NBANDS + band;
                 if ((lane & 15) == 0 && gband < a.nbands && q.tile_x < a.nhalves)
-                    a.part[(static_cast<size_t>(to) * a.nbands + gband) * a.nhalves + q.tile_x] = s;
-                if (lane == 0) atomic_max_nonneg(a.frame_max + to, __int_as_float(wm));
+                    a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gband) * a.nhalves + q.tile_x] = s;
+                if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
             }
         }
     }

@@ -306,8 +306,11 @@ struct sfseg_ctx {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
-    // resident problem
+    // resident problem. T = frames in the device buffers; for a time shard
+    // the buffer holds global frames [buf_t0, buf_t0 + T) of a Tg-frame
+    // problem and the rank outputs frames [out_t0, out_t1).
     int T = 0, H = 0, W = 0, P = 0, C = 0;
+    int Tg = 0, buf_t0 = 0, out_t0 = 0, out_t1 = 0, halo = 0;
     bool loaded = false;    // buffers allocated for (T, H, W, C)
     bool resident = false;  // a problem from sfseg_load is in S/F/x0
     bool has_x0 = false;
@@ -348,6 +351,11 @@ struct sfseg_ctx {
 
     size_t vol_elems() const { return static_cast<size_t>(T) * H * P; }
     Vol vol(float* p) const { return Vol{p, T, H, W, P}; }
+    int Tout() const { return out_t1 - out_t0; }
+    // the rank's output frames inside a buffer
+    Vol out_vol(float* p) const {
+        return Vol{p + static_cast<size_t>(out_t0 - buf_t0) * H * P, Tout(), H, W, P};
+    }
     int nbands() const { return (H + 3) / 4; }
     int nhalves() const { return (W + 31) / 32; }
 };
@@ -400,9 +408,19 @@ void check_shape(uint32_t T, uint32_t H, uint32_t W) {
         fail(SFSEG_ERR_CAPACITY, "volume shape exceeds the supported extent");
 }
 
-void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
-    if (c->loaded && c->T == (int)T && c->H == (int)H && c->W == (int)W && c->C == C) return;
+void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int Tg = -1,
+               int buf_t0 = 0, int out_t0 = 0, int out_t1 = -1, int halo = 0) {
+    if (Tg < 0) Tg = static_cast<int>(T);
+    if (out_t1 < 0) out_t1 = Tg;
+    if (c->loaded && c->T == (int)T && c->H == (int)H && c->W == (int)W && c->C == C &&
+        c->Tg == Tg && c->buf_t0 == buf_t0 && c->out_t0 == out_t0 && c->out_t1 == out_t1)
+        return;
     release_problem(c);
+    c->Tg = Tg;
+    c->buf_t0 = buf_t0;
+    c->out_t0 = out_t0;
+    c->out_t1 = out_t1;
+    c->halo = halo;
     c->T = T;
     c->H = H;
     c->W = W;
@@ -414,11 +432,12 @@ void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
     c->Fw = c->F;
     c->y[0] = dalloc_vol(c);
     c->y[1] = dalloc_vol(c);
-    c->part_elems = static_cast<size_t>(T) * c->nbands() * c->nhalves();
+    const int tout = c->Tout();
+    c->part_elems = static_cast<size_t>(tout) * c->nbands() * c->nhalves();
     ck(cudaMalloc(&c->part, c->part_elems * sizeof(double)), "cudaMalloc partials");
-    ck(cudaMalloc(&c->frame_sum, T * sizeof(double)), "cudaMalloc frame sums");
-    ck(cudaMalloc(&c->frame_max, T * sizeof(float)), "cudaMalloc frame max");
-    ck(cudaMemsetAsync(c->frame_max, 0, T * sizeof(float), c->stream), "memset");
+    ck(cudaMalloc(&c->frame_sum, std::max(tout, Tg) * sizeof(double)), "cudaMalloc frame sums");
+    ck(cudaMalloc(&c->frame_max, std::max(tout, Tg) * sizeof(float)), "cudaMalloc frame max");
+    ck(cudaMemsetAsync(c->frame_max, 0, std::max(tout, Tg) * sizeof(float), c->stream), "memset");
     c->loaded = true;
 }
 
@@ -551,26 +570,27 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         a.out = out;
         a.part = c->part;
         a.frame_max = c->frame_max;
+        a.part_t0 = c->out_t0;
         a.st = st;
         fill_taps(a, k, *v);
         a.inv_alpha = inv_alpha;
         a.one = 1.0f;
         a.zero = 0.0f;
-        a.T = c->T;
+        a.T = c->Tg;
         a.H = c->H;
         a.W = c->W;
         a.pitch = c->P;
-        a.buf_t0 = 0;
-        a.out_t0 = 0;
-        a.out_t1 = c->T;
-        a.out_buf_t0 = 0;
+        a.buf_t0 = c->buf_t0;
+        a.out_t0 = c->out_t0;
+        a.out_t1 = c->out_t1;
+        a.out_buf_t0 = c->buf_t0;
         a.tiles_x = (c->W + v->tx - 1) / v->tx;
         a.tiles_y = (c->H + v->ty - 1) / v->ty;
         a.nbands = c->nbands();
         a.nhalves = c->nhalves();
         const int ntiles = a.tiles_x * a.tiles_y;
         const int grid_n = c->num_sms;
-        upload_schedule(c, ntiles, c->T, grid_n);
+        upload_schedule(c, ntiles, c->Tout(), grid_n);
         a.sched = c->sched_seg;
         a.sched_off = c->sched_off;
         static bool attr_set[64] = {};
@@ -632,19 +652,24 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                                                   inv_alpha, ch == 0);
         launched(c->stream, "generic step");
     }
-    const long long warps = static_cast<long long>(c->T) * c->nbands() * c->nhalves();
+    const long long warps = static_cast<long long>(c->Tout()) * c->nbands() * c->nhalves();
     sfk::k_partials<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, c->stream>>>(
-        c->vol(out), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
+        c->out_vol(out), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
     launched(c->stream, "k_partials");
+}
+
+void frame_sums(sfseg_ctx* c) {
+    const int per_frame = c->nbands() * c->nhalves();
+    sfk::k_finalize_frames<<<c->Tout(), sfk::kAuxThreads, 0, c->stream>>>(c->part, per_frame,
+                                                                        c->frame_sum, 0);
+    launched(c->stream, "k_finalize_frames");
 }
 
 void finalize(sfseg_ctx* c, IterState* st, double* norms, int iter_index, int mode_next,
               double lambda, double frac) {
-    const int per_frame = c->nbands() * c->nhalves();
-    sfk::k_finalize_frames<<<c->T, sfk::kAuxThreads, 0, c->stream>>>(c->part, per_frame,
-                                                                   c->frame_sum, 0);
+    frame_sums(c);
     sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
-        c->frame_sum, c->frame_max, c->T, st, norms, iter_index, mode_next, lambda, frac);
+        c->frame_sum, c->frame_max, c->Tout(), st, norms, iter_index, mode_next, lambda, frac);
     launched(c->stream, "finalize");
 }
 
@@ -696,7 +721,7 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
         IterState s{};
         s.mode = 0;
         set_state(c, c->st, s);
-        ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
+        ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
         c->cur = -1;
     }
     for (auto e : c->ev) cudaEventDestroy(e);
@@ -788,8 +813,8 @@ void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
 
 void reduce_volume(sfseg_ctx* c, float* v, IterState* st, int mode_next, double lambda,
                    double frac) {
-    ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
-    const long long warps = static_cast<long long>(c->T) * c->nbands() * c->nhalves();
+    ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
+    const long long warps = static_cast<long long>(c->Tout()) * c->nbands() * c->nhalves();
     sfk::k_partials<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, c->stream>>>(
         c->vol(v), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
     launched(c->stream, "k_partials");
@@ -1054,7 +1079,7 @@ int sfseg_step(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
         IterState s{};
         s.mode = 0;
         set_state(c, c->st_aux, s);
-        ck(cudaMemsetAsync(c->frame_max, 0, c->T * sizeof(float), c->stream), "memset");
+        ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
         launch_step(c, k, p->alpha, xin, c->st_aux, c->y[0], c->F, p->arith == SFSEG_ARITH_FAST);
         download(c, out, c->y[0], mem);
         ck(cudaStreamSynchronize(c->stream), "sfseg_step");
@@ -1169,6 +1194,150 @@ int sfseg_convolve_separable(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, c
         download(c, out, a, mem);
         ck(cudaStreamSynchronize(c->stream), "convolve_separable");
         g_conv_count.fetch_add(1, std::memory_order_relaxed);
+    });
+}
+
+// ---- time-sharded solve ----------------------------------------------------
+
+int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int32_t out_t0,
+                     int32_t out_t1, int32_t halo, const float* S, const float* const* F,
+                     const float* x0, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        check_shape(T, H, W);
+        if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
+        if (!S || !F) fail(SFSEG_ERR_PARAMETER, "null input");
+        if (out_t0 < 0 || out_t1 <= out_t0 || out_t1 > static_cast<int>(T) || halo < 0)
+            fail(SFSEG_ERR_PARAMETER, "bad shard range");
+        if (out_t1 - out_t0 < halo && !(out_t0 == 0 && out_t1 == static_cast<int>(T)))
+            fail(SFSEG_ERR_PARAMETER, "a shard must own at least `halo` frames");
+        const int buf_t0 = std::max(0, out_t0 - halo);
+        const int buf_t1 = std::min(static_cast<int>(T), out_t1 + halo);
+        set_shape(c, buf_t1 - buf_t0, H, W, C, T, buf_t0, out_t0, out_t1, halo);
+        c->Fw = c->F;
+        c->guard_applied = false;
+        c->sp_p = NAN;
+        c->cur = -1;
+        upload(c, c->S, S, mem);
+        for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
+        validate_vol(c, c->S, true, "unary");
+        for (int i = 0; i < C; ++i) validate_vol(c, c->F[i], false, "pairwise");
+        c->has_x0 = x0 != nullptr;
+        if (x0) {
+            if (!c->x0) c->x0 = dalloc_vol(c);
+            upload(c, c->x0, x0, mem);
+            validate_vol(c, c->x0, true, "x0");
+        }
+        c->resident = true;
+    });
+}
+
+int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_shard_io* io) {
+    return guarded([&] {
+        if (!c || !io) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        validate_params(p);
+        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_shard_step before sfseg_shard_load");
+        if (iter > 1 && c->cur < 0) fail(SFSEG_ERR_STATE, "iteration 1 was not run");
+        if (p->radii[0] > c->halo) fail(SFSEG_ERR_PARAMETER, "kernel time radius exceeds the shard halo");
+        const HostKernel k = make_kernel(p->radii, p->sigmas);
+        // the unit-range guard needs global min/max: the sharded driver applies
+        // it to the channels before loading them (sharding.py)
+        ensure_sp(c, p->p);
+        if (iter == 1) {
+            IterState s{};
+            s.mode = 0;
+            set_state(c, c->st, s);
+            c->cur = -1;
+        }
+        ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
+        const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
+        const int dst = c->cur < 0 ? 0 : 1 - c->cur;
+        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST);
+        frame_sums(c);
+        c->cur = dst;
+        ck(cudaStreamSynchronize(c->stream), "shard step");
+        const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
+        float* y = c->y[dst];
+        const int buf_t1 = c->buf_t0 + c->T;
+        std::memset(io, 0, sizeof *io);
+        io->halo = c->halo;
+        io->out_frames = c->Tout();
+        if (c->out_t0 > 0) {
+            io->send_lo = y + (c->out_t0 - c->buf_t0) * fr;
+            io->send_lo_bytes = std::min(c->halo, c->Tout()) * fr * sizeof(float);
+            io->recv_lo = y;
+            io->recv_lo_bytes = (c->out_t0 - c->buf_t0) * fr * sizeof(float);
+        }
+        if (c->out_t1 < c->Tg) {
+            const int n = std::min(c->halo, c->Tout());
+            io->send_hi = y + (c->out_t1 - n - c->buf_t0) * fr;
+            io->send_hi_bytes = n * fr * sizeof(float);
+            io->recv_hi = y + (c->out_t1 - c->buf_t0) * fr;
+            io->recv_hi_bytes = (buf_t1 - c->out_t1) * fr * sizeof(float);
+        }
+        io->frame_sum = c->frame_sum;
+        io->frame_max = c->frame_max;
+    });
+}
+
+int sfseg_shard_finalize(sfseg_ctx* c, const sfseg_params* p, int32_t iter,
+                         const double* frame_sum, const float* frame_max, double* norm,
+                         int32_t mem) {
+    return guarded([&] {
+        if (!c || !frame_sum || !frame_max) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        validate_params(p);
+        const cudaMemcpyKind kind =
+            mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        ck(cudaMemcpyAsync(c->frame_sum, frame_sum, c->Tg * sizeof(double), kind, c->stream), "sums");
+        ck(cudaMemcpyAsync(c->frame_max, frame_max, c->Tg * sizeof(float), kind, c->stream), "max");
+        const int mode_next = iter >= p->binarize_start ? 2 : 1;
+        sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
+            c->frame_sum, c->frame_max, c->Tg, c->st, nullptr, 0, mode_next, lambda_for(p, iter),
+            p->threshold_frac);
+        launched(c->stream, "k_finalize_total");
+        const IterState s = get_state(c, c->st);
+        if (norm) *norm = s.norm;
+        if (s.norm == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+    });
+}
+
+int sfseg_shard_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, int32_t mem) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_shard_download before sfseg_shard_load");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        float* x = tmp_vol(c, 0);
+        materialize(c, x);
+        const Vol xo = c->out_vol(x);
+        const cudaMemcpyKind kind =
+            mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (soft)
+            ck(cudaMemcpy2DAsync(soft, c->W * sizeof(float), xo.p, c->P * sizeof(float),
+                                 c->W * sizeof(float), static_cast<size_t>(xo.T) * c->H, kind,
+                                 c->stream),
+               "download shard");
+        if (mask) {
+            // global max of the projected iterate comes from the shared state
+            if (c->cur < 0) fail(SFSEG_ERR_STATE, "no iteration has run");
+            sfk::k_state_max<<<1, 1, 0, c->stream>>>(c->st, c->scratch_f);
+            const size_t n = static_cast<size_t>(xo.T) * c->H * c->W;
+            uint8_t* dm = mem == SFSEG_MEM_DEVICE ? mask : nullptr;
+            if (!dm) ck(cudaMallocAsync(reinterpret_cast<void**>(&dm), n, c->stream), "malloc");
+            sfk::k_mask<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(xo, c->scratch_f, frac, dm);
+            launched(c->stream, "k_mask");
+            if (mem != SFSEG_MEM_DEVICE) {
+                ck(cudaMemcpyAsync(mask, dm, n, cudaMemcpyDeviceToHost, c->stream), "mask D2H");
+                ck(cudaFreeAsync(dm, c->stream), "free");
+            }
+        }
+        ck(cudaStreamSynchronize(c->stream), "shard download");
     });
 }
 

@@ -32,8 +32,9 @@ struct FusedArgs {
     const float* sp;            // pitched S^p (recombination reload)
     const float* f[kMaxCG];
     float* out;                 // pitched y_{k+1}
-    double* part;               // canonical partial sums [T][nbands][nhalves]
-    float* frame_max;           // [T] max(0, y_{k+1}) per frame (int-ordered)
+    double* part;               // canonical partial sums [Tout][nbands][nhalves]
+    float* frame_max;           // [Tout] max(0, y_{k+1}) per frame (int-ordered)
+    int part_t0;                // global frame of part/frame_max entry 0
     const IterState* st;
     float taps_x[kMaxTapsXY];
     float taps_y[kMaxTapsXY];

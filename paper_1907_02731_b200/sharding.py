@@ -1,0 +1,215 @@
+"""Time-sharded SFSeg solve across GPUs (one process per GPU, NCCL).
+
+The reference has no distributed backend (parallel.hpp is its
+only parallelism); its per-frame Jacobi sweep (engine.cpp:287-325) is what
+makes the time axis shardable: every frame of iterate k+1 depends only on
+frames t-rt..t+rt of iterate k. Rank r owns a contiguous range of output
+frames and keeps `halo` = rt frames of each neighbour:
+
+  per iteration
+    1. fused stencil on the rank's frames            (sfseg_shard_step)
+    2. exchange the rt edge frames of the new iterate (NCCL send/recv)
+    3. all-gather the per-frame canonical sums / max  (NCCL all-gather)
+    4. every rank reduces the frames in frame order   (sfseg_shard_finalize)
+
+Step 4 makes the norm, the projection scalars and therefore every iterate
+bit-identical for any number of ranks. The unit-range guard of run()
+(engine.cpp:254-259) needs the global min/max of each channel, so it is
+applied here with an all-reduce before the channels are loaded.
+
+A backend supplies steps 1, 4 and the device buffers; CudaBackend is the
+product (libsfseg_cuda.so). tests/ drive the same driver with a CPU oracle
+backend over gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+
+
+def shard_range(T: int, world: int, rank: int) -> Tuple[int, int]:
+    """Balanced contiguous frames [t0, t1) of rank `rank`."""
+    base, rem = divmod(T, world)
+    t0 = rank * base + min(rank, rem)
+    return t0, t0 + base + (1 if rank < rem else 0)
+
+
+def buffer_range(T: int, t0: int, t1: int, halo: int) -> Tuple[int, int]:
+    return max(0, t0 - halo), min(T, t1 + halo)
+
+
+class _DeviceView:
+    """Zero-copy torch view of device memory owned by libsfseg_cuda."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": (count,), "typestr": typestr, "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+def device_tensor(ptr, count: int, dtype="float32"):
+    import torch
+
+    if not ptr or count == 0:
+        return None
+    typestr = {"float32": "<f4", "float64": "<f8", "uint8": "|u1"}[dtype]
+    return torch.as_tensor(_DeviceView(int(ptr), int(count), typestr), device="cuda")
+
+
+@dataclass
+class StepIO:
+    send_lo: object
+    send_hi: object
+    recv_lo: object
+    recv_hi: object
+    frame_sum: object
+    frame_max: object
+
+
+class CudaBackend:
+    """Shard of the resident problem on one GPU (libsfseg_cuda shard API)."""
+
+    def __init__(self, device: int = 0):
+        from .engine import Context
+
+        self.ctx = Context(device)
+        self.lib = self.ctx._lib
+
+    def load(self, T, H, W, S_local, F_local, x0_local, t0, t1, halo):
+        import torch
+
+        self.T, self.H, self.W = T, H, W
+        self._keep = [S_local] + list(F_local) + ([x0_local] if x0_local is not None else [])
+        mem = N.SFSEG_MEM_DEVICE if isinstance(S_local, torch.Tensor) and S_local.is_cuda \
+            else N.SFSEG_MEM_HOST
+        ptr = lambda a: a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+        fp = (C.c_void_p * len(F_local))(*[ptr(f) for f in F_local])
+        N.check(self.lib.sfseg_shard_load(
+            self.ctx.handle, T, H, W, len(F_local), t0, t1, halo, C.c_void_p(ptr(S_local)),
+            C.cast(fp, C.c_void_p), C.c_void_p(ptr(x0_local)) if x0_local is not None else None,
+            mem))
+
+    def step(self, params, it) -> StepIO:
+        io = N.ShardIO()
+        N.check(self.lib.sfseg_shard_step(self.ctx.handle, C.byref(params), it, C.byref(io)))
+        f = lambda p, b: device_tensor(p, b // 4, "float32")
+        return StepIO(f(io.send_lo, io.send_lo_bytes), f(io.send_hi, io.send_hi_bytes),
+                      f(io.recv_lo, io.recv_lo_bytes), f(io.recv_hi, io.recv_hi_bytes),
+                      device_tensor(io.frame_sum, io.out_frames, "float64"),
+                      device_tensor(io.frame_max, io.out_frames, "float32"))
+
+    def finalize(self, params, it, frame_sum, frame_max) -> float:
+        norm = C.c_double()
+        N.check(self.lib.sfseg_shard_finalize(
+            self.ctx.handle, C.byref(params), it, C.c_void_p(frame_sum.data_ptr()),
+            C.c_void_p(frame_max.data_ptr()), C.byref(norm), N.SFSEG_MEM_DEVICE))
+        return norm.value
+
+    def download(self, frac, t0, t1):
+        soft = np.empty((t1 - t0, self.H, self.W), np.float32)
+        mask = np.empty((t1 - t0, self.H, self.W), np.uint8)
+        N.check(self.lib.sfseg_shard_download(self.ctx.handle, float(frac),
+                                              C.c_void_p(soft.ctypes.data),
+                                              C.c_void_p(mask.ctypes.data), N.SFSEG_MEM_HOST))
+        return soft, mask
+
+    def synchronize(self):
+        import torch
+
+        torch.cuda.synchronize()
+
+    def close(self):
+        self.ctx.close()
+
+
+def global_unit_range_guard(F_local: Sequence, group=None) -> None:
+    """scale_channel_into_unit_range (engine.cpp:228-243) with the channel's
+    global min/max (all-reduce), applied in place to each rank's frames."""
+    import torch
+    import torch.distributed as dist
+
+    for f in F_local:
+        t = f if isinstance(f, torch.Tensor) else torch.from_numpy(f)
+        lo = t.min().reshape(1).clone()
+        hi = t.max().reshape(1).clone()
+        if dist.is_initialized():
+            dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+            dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+        lo_v, hi_v = float(lo.item()), float(hi.item())
+        if lo_v >= 0.0 and hi_v <= 1.0:
+            continue  # leave the bits alone
+        if hi_v > lo_v:
+            span = torch.tensor(hi_v, dtype=torch.float32) - torch.tensor(lo_v, dtype=torch.float32)
+            t.sub_(torch.tensor(lo_v, dtype=torch.float32, device=t.device)).div_(span.to(t.device))
+        else:
+            t.fill_(min(max(lo_v, 0.0), 1.0))
+
+
+class ShardedSolver:
+    """Runs Algorithm 1 over `world` ranks of a process group."""
+
+    def __init__(self, backend, rank: int, world: int, group=None):
+        self.b = backend
+        self.rank, self.world, self.group = rank, world, group
+
+    def load(self, T, H, W, S_local, F_local, x0_local, halo, guard=True):
+        self.T, self.H, self.W, self.halo = T, H, W, halo
+        self.t0, self.t1 = shard_range(T, self.world, self.rank)
+        if guard:
+            global_unit_range_guard(F_local, self.group)
+        self.b.load(T, H, W, S_local, F_local, x0_local, self.t0, self.t1, halo)
+        self.tmax = max(shard_range(T, self.world, r)[1] - shard_range(T, self.world, r)[0]
+                        for r in range(self.world))
+
+    def _exchange(self, io: StepIO):
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return
+        ops = []
+        if io.send_lo is not None:  # my first frames -> rank-1's upper halo
+            ops.append(dist.P2POp(dist.isend, io.send_lo, self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, io.recv_lo, self.rank - 1, self.group))
+        if io.send_hi is not None:
+            ops.append(dist.P2POp(dist.isend, io.send_hi, self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, io.recv_hi, self.rank + 1, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def _gather(self, local, dtype):
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return local
+        pad = torch.zeros(self.tmax, dtype=dtype, device=local.device)
+        pad[: local.numel()] = local
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(bufs, pad, group=self.group)
+        parts = []
+        for r in range(self.world):
+            a, b = shard_range(self.T, self.world, r)
+            parts.append(bufs[r][: b - a])
+        return torch.cat(parts).contiguous()  # frame order
+
+    def run(self, cfg) -> Tuple[np.ndarray, np.ndarray, List[float]]:
+        import torch
+
+        params = cfg.to_params()
+        self.b.cfg = cfg
+        norms = []
+        for it in range(1, cfg.iterations + 1):
+            io = self.b.step(params, it)
+            self._exchange(io)
+            fs = self._gather(io.frame_sum, torch.float64)
+            fm = self._gather(io.frame_max, torch.float32)
+            self.b.synchronize()
+            norms.append(self.b.finalize(params, it, fs, fm))
+        soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1)
+        return soft, mask, norms

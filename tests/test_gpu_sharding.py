@@ -1,0 +1,55 @@
+"""CUDA shard API (sfseg_shard_*) on one GPU: two shard contexts stand in for
+two ranks; the host copies the halos and concatenates the per-frame sums the
+way NCCL send/recv + all-gather do in sharding.py. No kernel waits on
+another (the exchange is host-driven), so this is a faithful single-GPU test
+of the multi-GPU data path. The sharded result must equal the single-context
+solve bit for bit."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1907_02731_b200 import engine as E
+from paper_1907_02731_b200 import synth
+from paper_1907_02731_b200.sharding import CudaBackend, buffer_range, shard_range
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,arith,binarize", [(2, "exact", False), (3, "fast", True)])
+def test_shards_match_single_context(world, arith, binarize):
+    prob = synth.config(1, frames=12)[0]
+    fs, _ = prob.generate()
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, "iterations": 6,
+                           "binarize_start": 3 if binarize else 7})
+    T, H, W = prob.shape
+    halo = cfg.kernel.radii[0]
+    ranks = []
+    for r in range(world):
+        t0, t1 = shard_range(T, world, r)
+        b0, b1 = buffer_range(T, t0, t1, halo)
+        be = CudaBackend(0)
+        be.load(T, H, W, np.ascontiguousarray(fs.unary[b0:b1]),
+                [np.ascontiguousarray(f[b0:b1]) for f in fs.pairwise], None, t0, t1, halo)
+        be.cfg = cfg
+        ranks.append((be, t0, t1))
+    params = cfg.to_params()
+    norms = []
+    for it in range(1, cfg.iterations + 1):
+        ios = [be.step(params, it) for be, _, _ in ranks]
+        for r in range(world - 1):  # halo exchange between neighbours
+            ios[r + 1].recv_lo.copy_(ios[r].send_hi)
+            ios[r].recv_hi.copy_(ios[r + 1].send_lo)
+        fsum = torch.cat([io.frame_sum for io in ios]).contiguous()
+        fmax = torch.cat([io.frame_max for io in ios]).contiguous()
+        torch.cuda.synchronize()
+        n = [be.finalize(params, it, fsum, fmax) for be, _, _ in ranks]
+        assert len(set(n)) == 1
+        norms.append(n[0])
+    soft = np.concatenate([be.download(cfg.final_threshold, a, b)[0] for be, a, b in ranks])
+    mask = np.concatenate([be.download(cfg.final_threshold, a, b)[1] for be, a, b in ranks])
+    ref = E.run(fs, cfg)
+    assert np.array_equal(soft, ref.soft)
+    assert np.array_equal(mask, ref.mask)
+    assert np.array_equal(norms, [r.l2_norm_pre_normalize for r in ref.trace.iterations])
+    for be, _, _ in ranks:
+        be.close()
