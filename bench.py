@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-frames", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the time-sharded driver even on one GPU (testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -212,76 +214,122 @@ def main():
     nvox = T * H * W
     iters = cfg.iterations
 
-    # pinned host inputs, generated once
+    # pinned host inputs, generated once (every rank generates the same seeded
+    # problem and keeps its frames)
     S = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
     F = [torch.empty((T, H, W), dtype=torch.float32, pin_memory=True) for _ in range(Cn)]
     prob.generate(out=(S.numpy(), [f.numpy() for f in F]))
 
-    ctx = E.Context(local)
-    lib = ctx._lib
-    p = cfg.to_params()
-    fptrs = (C.c_void_p * Cn)(*[f.data_ptr() for f in F])
-    # device-resident load (H2D once, outside the timed region)
-    N.check(lib.sfseg_load(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
-                           C.cast(fptrs, C.c_void_p), None, N.SFSEG_MEM_HOST))
-
     def barrier():
         torch.cuda.synchronize()
-        ctx.synchronize()
         if dist:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-    ctx.set_timing(True)
-    barrier()
-    solve_ms, kern_ms, launches = [], 0.0, 0
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
+    clocks = ClockSampler(local)
+    if world == 1 and not args.sharded:
+        ctx = E.Context(local)
+        lib = ctx._lib
+        p = cfg.to_params()
+        fptrs = (C.c_void_p * Cn)(*[f.data_ptr() for f in F])
+        # device-resident load (H2D once, outside the timed region)
+        N.check(lib.sfseg_load(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
+                               C.cast(fptrs, C.c_void_p), None, N.SFSEG_MEM_HOST))
+        for _ in range(args.warmup):
             N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-            tm = ctx.timing()
-            solve_ms.append(tm.solve_ms)
-            kern_ms += tm.step_kernel_ms
-            launches += tm.step_launches
-    barrier()
-    ctx.set_timing(False)
-    total_ms = sum(solve_ms)
+        ctx.set_timing(True)
+        ctx.synchronize()
+        barrier()
+        solve_ms, kern_ms, launches = [], 0.0, 0
+        with clocks:
+            for _ in range(args.steps):
+                N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
+                tm = ctx.timing()
+                solve_ms.append(tm.solve_ms)
+                kern_ms += tm.step_kernel_ms
+                launches += tm.step_launches
+        ctx.synchronize()
+        barrier()
+        ctx.set_timing(False)
+        total_ms = sum(solve_ms)
+        avg_launch_ms = kern_ms / max(1, launches)
+    else:
+        # time-sharded: rank r owns frames [t0, t1) plus rt halo frames
+        from paper_1907_02731_b200.sharding import (CudaBackend, ShardedSolver, buffer_range,
+                                                    shard_range)
+
+        halo = cfg.kernel.radii[0]
+        be = CudaBackend(local)
+        solver = ShardedSolver(be, rank, world)
+        t0, t1 = shard_range(T, world, rank)
+        b0, b1 = buffer_range(T, t0, t1, halo)
+        dS = S[b0:b1].cuda()
+        dF = [f[b0:b1].cuda() for f in F]
+        solver.load(T, H, W, dS, dF, None, halo)
+        for _ in range(args.warmup):
+            solver.solve_only(cfg)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with clocks:
+            ev0.record()
+            be.after_exchange()  # the library stream starts after ev0
+            for _ in range(args.steps):
+                solver.solve_only(cfg)
+            be.before_exchange()  # current stream waits for the library stream
+            ev1.record()
+            torch.cuda.synchronize()
+        total_ms = ev0.elapsed_time(ev1)
+        barrier()
+        avg_launch_ms = float("nan")
     if dist:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * nvox * iters * args.steps / (total_ms * 1e-3)
+    value = nvox * iters * args.steps / (total_ms * 1e-3)
 
     # roofline of the dominant kernel (fused stencil): algorithmic bytes per
-    # launch = 4 B x (x, S^p, F_c reads + one write) per voxel
-    bytes_per_launch = 4.0 * (Cn + 3) * nvox if Cn == 1 else 4.0 * (4) * nvox
-    avg_launch_ms = kern_ms / max(1, launches)
-    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    # launch = 4 B x (x, S^p, F_c reads + one write) per voxel, one launch per
+    # channel group
+    bytes_per_launch = 4.0 * (Cn + 3) * nvox if Cn == 1 else 4.0 * 4 * nvox
+    sharded = world > 1 or args.sharded
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9 if not sharded else float("nan")
     peak, peak_kind = _peaks()
     traffic = None
     tfile = ROOT / "profiles" / f"traffic_c{args.config}_{args.arith}.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
 
-    # end to end: public C ABI sfseg_run from pinned host memory, per step
-    soft = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
-    mask = torch.empty((T, H, W), dtype=torch.uint8, pin_memory=True)
+    # end to end through the public C ABI from pinned host memory, per step
     e2e_t = []
-    for i in range(args.e2e_steps + 1):
-        barrier()
-        t0 = time.perf_counter()
-        N.check(lib.sfseg_run(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
-                              C.cast(fptrs, C.c_void_p), None, C.byref(p),
-                              C.c_void_p(soft.data_ptr()), C.c_void_p(mask.data_ptr()), None,
-                              N.SFSEG_MEM_HOST))
-        if i > 0:  # first call warms the path
-            e2e_t.append(time.perf_counter() - t0)
+    if not sharded:
+        soft = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
+        mask = torch.empty((T, H, W), dtype=torch.uint8, pin_memory=True)
+        for i in range(args.e2e_steps + 1):
+            barrier()
+            t_0 = time.perf_counter()
+            N.check(lib.sfseg_run(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
+                                  C.cast(fptrs, C.c_void_p), None, C.byref(p),
+                                  C.c_void_p(soft.data_ptr()), C.c_void_p(mask.data_ptr()), None,
+                                  N.SFSEG_MEM_HOST))
+            if i > 0:  # first call warms the path
+                e2e_t.append(time.perf_counter() - t_0)
+        h2d = (1 + Cn) * nvox * 4
+        d2h = nvox * 4 + nvox
+    else:
+        for i in range(args.e2e_steps + 1):
+            barrier()
+            t_0 = time.perf_counter()
+            solver.load(T, H, W, S[b0:b1], [f[b0:b1] for f in F], None, halo)
+            solver.run(cfg)
+            if i > 0:
+                e2e_t.append(time.perf_counter() - t_0)
+        h2d = (1 + Cn) * (b1 - b0) * H * W * 4 * world
+        d2h = (t1 - t0) * H * W * 5 * world
     e2e_s = sum(e2e_t) / len(e2e_t)
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * nvox * iters / e2e_s
+    e2e_value = nvox * iters / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -300,7 +348,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"BASELINE configs[{args.config}] ({prob.name})",
                        "shape": [T, H, W], "channels": Cn, "radii": list(cfg.kernel.radii),
@@ -308,7 +356,8 @@ def main():
                        "alpha": cfg.alpha, "p": cfg.p, "binarization": "off",
                        "arith": args.arith,
                        "l2": f"inputs larger than L2 ({(Cn + 2) * nvox * 4 / 1e6:.0f} MB read per iteration)",
-                       "parallelism": f"replicas{world}" if world > 1 else "single"},
+                       "parallelism": f"time-sharded x{world} (rt-frame halos, NCCL)"
+                       if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
@@ -316,13 +365,15 @@ def main():
                          "bytes_per_launch": bytes_per_launch},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": (1 + Cn) * nvox * 4,
-                    "d2h_bytes_per_step": nvox * 4 + nvox},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * iters * (Cn + 2),
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
+    if not sharded:
+        ctx.close()
+    else:
+        be.close()
     if dist:
         dist.destroy_process_group()
 

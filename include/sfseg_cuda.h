@@ -127,6 +127,8 @@ int sfseg_ctx_set_timing(sfseg_ctx* ctx, int enabled);
 int sfseg_ctx_get_timing(const sfseg_ctx* ctx, sfseg_timing* out);
 /* Blocks until the context stream is idle. */
 int sfseg_ctx_synchronize(sfseg_ctx* ctx);
+/* The context's cudaStream_t (as void*), for ordering NCCL work against it. */
+void* sfseg_ctx_stream(sfseg_ctx* ctx);
 
 /* ---- resident problem (run(), engine.cpp:247-348) ----------------------- */
 
@@ -234,11 +236,18 @@ int sfseg_shard_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t 
                      int32_t channels, int32_t out_t0, int32_t out_t1, int32_t halo,
                      const float* unary, const float* const* pairwise, const float* x0,
                      int32_t mem);
+/* Enqueues the step on the context stream (asynchronous: order the exchange
+ * after it, e.g. with sfseg_ctx_stream + a stream wait). */
 int sfseg_shard_step(sfseg_ctx* ctx, const sfseg_params* p, int32_t iter, sfseg_shard_io* io);
-/* frame_sum / frame_max: global [frames] arrays (device or host, per mem). */
+/* frame_sum / frame_max: global [frames] arrays (device or host, per mem).
+ * Asynchronous when norm == NULL (the norm is kept for sfseg_shard_norms);
+ * otherwise blocks and returns it. */
 int sfseg_shard_finalize(sfseg_ctx* ctx, const sfseg_params* p, int32_t iter,
                          const double* frame_sum, const float* frame_max, double* norm,
                          int32_t mem);
+/* Norms of iterations 1..count of the current sharded solve (blocks);
+ * SFSEG_ERR_DEGENERATE if any is zero. */
+int sfseg_shard_norms(sfseg_ctx* ctx, int32_t count, double* norms);
 /* Soft iterate / mask of the rank's output frames; frac as threshold_final. */
 int sfseg_shard_download(sfseg_ctx* ctx, double frac, float* soft, uint8_t* mask, int32_t mem);
 

@@ -139,6 +139,7 @@ _SIGS = {
     "sfseg_ctx_set_timing": (C.c_int, [_P, C.c_int]),
     "sfseg_ctx_get_timing": (C.c_int, [_P, C.POINTER(Timing)]),
     "sfseg_ctx_synchronize": (C.c_int, [_P]),
+    "sfseg_ctx_stream": (C.c_void_p, [_P]),
     "sfseg_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, _I32]),
     "sfseg_solve": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, C.POINTER(IterRecord)]),
     "sfseg_download": (C.c_int, [_P, C.c_double, _P, _P, _I32]),
@@ -159,6 +160,7 @@ _SIGS = {
     "sfseg_shard_finalize": (C.c_int, [_P, C.POINTER(Params), _I32, _P, _P,
                                        C.POINTER(C.c_double), _I32]),
     "sfseg_shard_download": (C.c_int, [_P, C.c_double, _P, _P, _I32]),
+    "sfseg_shard_norms": (C.c_int, [_P, _I32, C.POINTER(C.c_double)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -955,6 +955,8 @@ int sfseg_ctx_get_timing(const sfseg_ctx* c, sfseg_timing* out) {
     });
 }
 
+void* sfseg_ctx_stream(sfseg_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
 int sfseg_ctx_synchronize(sfseg_ctx* c) {
     return guarded([&] {
         if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
@@ -1259,7 +1261,6 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
         launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST);
         frame_sums(c);
         c->cur = dst;
-        ck(cudaStreamSynchronize(c->stream), "shard step");
         const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
         float* y = c->y[dst];
         const int buf_t1 = c->buf_t0 + c->T;
@@ -1297,13 +1298,42 @@ int sfseg_shard_finalize(sfseg_ctx* c, const sfseg_params* p, int32_t iter,
         ck(cudaMemcpyAsync(c->frame_sum, frame_sum, c->Tg * sizeof(double), kind, c->stream), "sums");
         ck(cudaMemcpyAsync(c->frame_max, frame_max, c->Tg * sizeof(float), kind, c->stream), "max");
         const int mode_next = iter >= p->binarize_start ? 2 : 1;
+        if (c->norms_cap < iter) {
+            double* nn = nullptr;
+            const int cap = std::max(64, 2 * iter);
+            ck(cudaMalloc(&nn, cap * sizeof(double)), "cudaMalloc norms");
+            if (c->norms) {
+                ck(cudaMemcpyAsync(nn, c->norms, c->norms_cap * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream), "norms");
+                ck(cudaStreamSynchronize(c->stream), "norms");
+                cudaFree(c->norms);
+            }
+            c->norms = nn;
+            c->norms_cap = cap;
+        }
         sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
-            c->frame_sum, c->frame_max, c->Tg, c->st, nullptr, 0, mode_next, lambda_for(p, iter),
-            p->threshold_frac);
+            c->frame_sum, c->frame_max, c->Tg, c->st, c->norms, iter - 1, mode_next,
+            lambda_for(p, iter), p->threshold_frac);
         launched(c->stream, "k_finalize_total");
-        const IterState s = get_state(c, c->st);
-        if (norm) *norm = s.norm;
-        if (s.norm == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+        if (norm) {
+            const IterState s = get_state(c, c->st);
+            *norm = s.norm;
+            if (s.norm == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+        }
+    });
+}
+
+int sfseg_shard_norms(sfseg_ctx* c, int32_t count, double* norms) {
+    return guarded([&] {
+        if (!c || !norms) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (count < 0 || count > c->norms_cap) fail(SFSEG_ERR_PARAMETER, "bad norm count");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaMemcpyAsync(norms, c->norms, count * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream), "norms");
+        ck(cudaStreamSynchronize(c->stream), "norms");
+        for (int i = 0; i < count; ++i)
+            if (norms[i] == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
     });
 }
 

@@ -76,10 +76,17 @@ class CudaBackend:
     """Shard of the resident problem on one GPU (libsfseg_cuda shard API)."""
 
     def __init__(self, device: int = 0):
+        import torch
+
         from .engine import Context
 
         self.ctx = Context(device)
         self.lib = self.ctx._lib
+        # the library's stream, so NCCL (on torch's stream) can be ordered
+        # against the kernels without host synchronisation
+        self.stream = torch.cuda.ExternalStream(self.lib.sfseg_ctx_stream(self.ctx.handle),
+                                                device=torch.device("cuda", device))
+        self._keep_gathered = []
 
     def load(self, T, H, W, S_local, F_local, x0_local, t0, t1, halo):
         import torch
@@ -104,12 +111,27 @@ class CudaBackend:
                       device_tensor(io.frame_sum, io.out_frames, "float64"),
                       device_tensor(io.frame_max, io.out_frames, "float32"))
 
-    def finalize(self, params, it, frame_sum, frame_max) -> float:
-        norm = C.c_double()
+    def before_exchange(self):
+        import torch
+
+        torch.cuda.current_stream().wait_stream(self.stream)
+
+    def after_exchange(self):
+        import torch
+
+        self.stream.wait_stream(torch.cuda.current_stream())
+
+    def finalize(self, params, it, frame_sum, frame_max) -> None:
+        self._keep_gathered.append((frame_sum, frame_max))  # alive until the stream passes
         N.check(self.lib.sfseg_shard_finalize(
             self.ctx.handle, C.byref(params), it, C.c_void_p(frame_sum.data_ptr()),
-            C.c_void_p(frame_max.data_ptr()), C.byref(norm), N.SFSEG_MEM_DEVICE))
-        return norm.value
+            C.c_void_p(frame_max.data_ptr()), None, N.SFSEG_MEM_DEVICE))
+
+    def norms(self, count):
+        out = (C.c_double * count)()
+        N.check(self.lib.sfseg_shard_norms(self.ctx.handle, count, out))
+        self._keep_gathered.clear()
+        return list(out)
 
     def download(self, frac, t0, t1):
         soft = np.empty((t1 - t0, self.H, self.W), np.float32)
@@ -118,11 +140,6 @@ class CudaBackend:
                                               C.c_void_p(soft.ctypes.data),
                                               C.c_void_p(mask.ctypes.data), N.SFSEG_MEM_HOST))
         return soft, mask
-
-    def synchronize(self):
-        import torch
-
-        torch.cuda.synchronize()
 
     def close(self):
         self.ctx.close()
@@ -203,13 +220,29 @@ class ShardedSolver:
 
         params = cfg.to_params()
         self.b.cfg = cfg
-        norms = []
         for it in range(1, cfg.iterations + 1):
             io = self.b.step(params, it)
+            self.b.before_exchange()
             self._exchange(io)
             fs = self._gather(io.frame_sum, torch.float64)
             fm = self._gather(io.frame_max, torch.float32)
-            self.b.synchronize()
-            norms.append(self.b.finalize(params, it, fs, fm))
+            self.b.after_exchange()
+            self.b.finalize(params, it, fs, fm)
+        norms = self.b.norms(cfg.iterations)
         soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1)
         return soft, mask, norms
+
+    def solve_only(self, cfg) -> None:
+        """The iteration loop without the download (benchmark timing)."""
+        import torch
+
+        params = cfg.to_params()
+        self.b.cfg = cfg
+        for it in range(1, cfg.iterations + 1):
+            io = self.b.step(params, it)
+            self.b.before_exchange()
+            self._exchange(io)
+            fs = self._gather(io.frame_sum, torch.float64)
+            fm = self._gather(io.frame_max, torch.float32)
+            self.b.after_exchange()
+            self.b.finalize(params, it, fs, fm)

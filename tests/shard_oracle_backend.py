@@ -75,6 +75,15 @@ class OracleBackend:
                       v(b, self.b1 - self.b0) if self.t1 < self.T else None,
                       torch.from_numpy(self.frame_sum), torch.from_numpy(self.frame_max))
 
+    def before_exchange(self):
+        pass
+
+    def after_exchange(self):
+        pass
+
+    def norms(self, count):
+        return self._norms[:count]
+
     def finalize(self, params, it, frame_sum, frame_max):
         cfg = self.cfg
         norm = math.sqrt(finalize_order_sum(frame_sum.numpy()))
@@ -87,7 +96,9 @@ class OracleBackend:
         lam = cfg.sigmoid_slope0 * cfg.slope_growth ** (it - cfg.binarize_start)
         self.state = dict(mode=mode, inv=inv, theta=cfg.threshold_frac * max_unit, lam=lam,
                           max_unit=max_unit)
-        return norm
+        if it == 1:
+            self._norms = []
+        self._norms.append(norm)
 
     def download(self, frac, t0, t1):
         a, b = self.t0 - self.b0, self.t1 - self.b0
@@ -99,5 +110,3 @@ class OracleBackend:
         cut = np.float32(frac * float(m))
         return x, (x > cut).astype(np.uint8)
 
-    def synchronize(self):
-        pass

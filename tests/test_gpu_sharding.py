@@ -36,15 +36,19 @@ def test_shards_match_single_context(world, arith, binarize):
     norms = []
     for it in range(1, cfg.iterations + 1):
         ios = [be.step(params, it) for be, _, _ in ranks]
+        for be, _, _ in ranks:
+            be.before_exchange()
         for r in range(world - 1):  # halo exchange between neighbours
             ios[r + 1].recv_lo.copy_(ios[r].send_hi)
             ios[r].recv_hi.copy_(ios[r + 1].send_lo)
         fsum = torch.cat([io.frame_sum for io in ios]).contiguous()
         fmax = torch.cat([io.frame_max for io in ios]).contiguous()
-        torch.cuda.synchronize()
-        n = [be.finalize(params, it, fsum, fmax) for be, _, _ in ranks]
-        assert len(set(n)) == 1
-        norms.append(n[0])
+        for be, _, _ in ranks:
+            be.after_exchange()
+            be.finalize(params, it, fsum, fmax)
+    per_rank = [be.norms(cfg.iterations) for be, _, _ in ranks]
+    assert all(p == per_rank[0] for p in per_rank)
+    norms = per_rank[0]
     soft = np.concatenate([be.download(cfg.final_threshold, a, b)[0] for be, a, b in ranks])
     mask = np.concatenate([be.download(cfg.final_threshold, a, b)[1] for be, a, b in ranks])
     ref = E.run(fs, cfg)
