@@ -198,6 +198,21 @@ int sfseg_convolve_separable(sfseg_ctx* ctx, uint32_t frames, uint32_t height,
                              uint32_t width, const float* v, const int32_t radii[3],
                              const double sigmas[3], float* out, int32_t mem);
 
+/* convolve_separable with explicit fp64 taps (a SeparableKernel3D, conv3d.hpp:
+ * 28-51): taps are cast to float per axis as conv3d.cpp:84-85 does. Each
+ * taps_* array holds 2*radius+1 values. */
+int sfseg_convolve_separable_taps(sfseg_ctx* ctx, uint32_t frames, uint32_t height,
+                                  uint32_t width, const float* v, const int32_t radii[3],
+                                  const double* taps_t, const double* taps_y,
+                                  const double* taps_x, float* out, int32_t mem);
+
+/* convolve_direct (conv3d.cpp:187-243): the dense triple sum in fp64 with
+ * the reference's weight products and summation order, then cast to float. */
+int sfseg_convolve_direct_taps(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                               const float* v, const int32_t radii[3], const double* taps_t,
+                               const double* taps_y, const double* taps_x, float* out,
+                               int32_t mem);
+
 /* Number of logical separable convolutions performed by this library since
  * load (separable_convolution_count, conv3d.cpp:64-66): 1 + 2C fields per
  * channel-step are counted as 3 per channel, as the reference does. */

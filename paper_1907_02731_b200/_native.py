@@ -155,6 +155,10 @@ _SIGS = {
     "sfseg_convolve_separable": (C.c_int, [_P, _U32, _U32, _U32, _P, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_double), _P, _I32]),
     "sfseg_separable_convolution_count": (C.c_uint64, []),
+    "sfseg_convolve_separable_taps": (C.c_int, [_P, _U32, _U32, _U32, _P, C.POINTER(C.c_int32),
+                                                _P, _P, _P, _P, _I32]),
+    "sfseg_convolve_direct_taps": (C.c_int, [_P, _U32, _U32, _U32, _P, C.POINTER(C.c_int32),
+                                             _P, _P, _P, _P, _I32]),
     "sfseg_shard_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32]),
     "sfseg_shard_step": (C.c_int, [_P, C.POINTER(Params), _I32, C.POINTER(ShardIO)]),
     "sfseg_shard_finalize": (C.c_int, [_P, C.POINTER(Params), _I32, _P, _P,

@@ -294,6 +294,35 @@ struct Taps {
     int rt, ry, rx;
 };
 
+// convolve_direct (conv3d.cpp:187-243): w = (taps_t * taps_y) * taps_x in
+// fp64, acc += w * src over dt, dy, dx ascending, skipping out-of-range
+// offsets; separately rounded (the reference build has no FMA)
+struct TapsD {
+    double t[32], y[32], x[32];
+    int rt, ry, rx;
+};
+
+__global__ void k_conv_direct(Vol in, Vol out, const __grid_constant__ TapsD k) {
+    SFK_FOR_VOXELS(in, t, y, x) {
+        double acc = 0.0;
+        for (int dt = -k.rt; dt <= k.rt; ++dt) {
+            const int tt = t + dt;
+            if (tt < 0 || tt >= in.T) continue;
+            for (int dy = -k.ry; dy <= k.ry; ++dy) {
+                const int yy = y + dy;
+                if (yy < 0 || yy >= in.H) continue;
+                for (int dx = -k.rx; dx <= k.rx; ++dx) {
+                    const int xx = x + dx;
+                    if (xx < 0 || xx >= in.W) continue;
+                    const double w = __dmul_rn(__dmul_rn(k.t[dt + k.rt], k.y[dy + k.ry]), k.x[dx + k.rx]);
+                    acc = __dadd_rn(acc, __dmul_rn(w, static_cast<double>(in.p[in.at(tt, yy, xx)])));
+                }
+            }
+        }
+        out.p[out.at(t, y, x)] = static_cast<float>(acc);
+    }
+}
+
 // products u, fu, f2u (engine.cpp:92-100) with the load transform
 __global__ void k_products(Vol xsrc, Vol sp, Vol f, Vol u, Vol fu, Vol f2u,
                            const IterState* stp) {

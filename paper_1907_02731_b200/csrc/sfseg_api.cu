@@ -1199,6 +1199,64 @@ int sfseg_convolve_separable(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, c
     });
 }
 
+int sfseg_convolve_separable_taps(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W,
+                                  const float* v, const int32_t radii[3], const double* tt,
+                                  const double* ty, const double* tx, float* out, int32_t mem) {
+    return guarded([&] {
+        if (!c || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
+        for (int i = 0; i < 3; ++i)
+            if (radii[i] < 0 || radii[i] > 31) fail(SFSEG_ERR_CAPACITY, "kernel radius above 31");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        sfk::Taps tp;
+        std::memset(&tp, 0, sizeof tp);
+        for (int i = 0; i <= 2 * radii[0]; ++i) tp.t[i] = static_cast<float>(tt[i]);
+        for (int i = 0; i <= 2 * radii[1]; ++i) tp.y[i] = static_cast<float>(ty[i]);
+        for (int i = 0; i <= 2 * radii[2]; ++i) tp.x[i] = static_cast<float>(tx[i]);
+        tp.rt = radii[0];
+        tp.ry = radii[1];
+        tp.rx = radii[2];
+        float *a = c->y[0], *b = c->y[1], *t0 = tmp_vol(c, 0);
+        upload(c, a, v, mem);
+        const int g = aux_grid(c), bt = sfk::kAuxThreads;
+        sfk::k_pass_x<<<g, bt, 0, c->stream>>>(c->vol(a), c->vol(t0), tp);
+        sfk::k_pass_y<<<g, bt, 0, c->stream>>>(c->vol(t0), c->vol(b), tp);
+        sfk::k_pass_t<<<g, bt, 0, c->stream>>>(c->vol(b), c->vol(a), tp);
+        launched(c->stream, "convolve_separable");
+        download(c, out, a, mem);
+        ck(cudaStreamSynchronize(c->stream), "convolve_separable");
+        g_conv_count.fetch_add(1, std::memory_order_relaxed);
+    });
+}
+
+int sfseg_convolve_direct_taps(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* v,
+                               const int32_t radii[3], const double* tt, const double* ty,
+                               const double* tx, float* out, int32_t mem) {
+    return guarded([&] {
+        if (!c || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
+        for (int i = 0; i < 3; ++i)
+            if (radii[i] < 0 || radii[i] > 15) fail(SFSEG_ERR_CAPACITY, "direct kernel radius above 15");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        sfk::TapsD tp;
+        std::memset(&tp, 0, sizeof tp);
+        for (int i = 0; i <= 2 * radii[0]; ++i) tp.t[i] = tt[i];
+        for (int i = 0; i <= 2 * radii[1]; ++i) tp.y[i] = ty[i];
+        for (int i = 0; i <= 2 * radii[2]; ++i) tp.x[i] = tx[i];
+        tp.rt = radii[0];
+        tp.ry = radii[1];
+        tp.rx = radii[2];
+        upload(c, c->y[0], v, mem);
+        sfk::k_conv_direct<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->y[0]),
+                                                                          c->vol(c->y[1]), tp);
+        launched(c->stream, "convolve_direct");
+        download(c, out, c->y[1], mem);
+        ck(cudaStreamSynchronize(c->stream), "convolve_direct");
+    });
+}
+
 // ---- time-sharded solve ----------------------------------------------------
 
 int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int32_t out_t0,
