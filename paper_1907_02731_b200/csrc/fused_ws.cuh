@@ -172,8 +172,16 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
             const float* rs = raw + static_cast<size_t>(s) * NIN * FB;
             // products over the halo box (engine.cpp:92-100), 4 points per item
+            // items i = tid, tid+NA, ...: (row, float4 column) advanced incrementally
+            int pr = tid / BW4, pc4 = tid - (tid / BW4) * BW4;
             for (int i = tid; i < BH * BW4; i += NA) {
-                const int r = i / BW4, c4 = i - r * BW4;
+                const int r = pr, c4 = pc4;
+                pr += NA / BW4;
+                pc4 += NA % BW4;
+                if (pc4 >= BW4) {
+                    pc4 -= BW4;
+                    ++pr;
+                }
                 const float4 yv = reinterpret_cast<const float4*>(rs)[i];
                 const float4 sv = reinterpret_cast<const float4*>(rs + FB)[i];
                 float4 xv;
@@ -231,8 +239,15 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             // the first NA/2 threads take the u strips, the others the pair
             // strips (equal counts and costs); lanes take consecutive rows
             if (tid < NA / 2) {
+                int xr = tid % BH, xs = tid / BH;  // strip (row, index), advanced incrementally
                 for (int it = tid; it < G::XU_ITEMS; it += NA / 2) {
-                    const int r = it % BH, sidx = it / BH;
+                    const int r = xr, sidx = xs;
+                    xr += (NA / 2) % BH;
+                    xs += (NA / 2) / BH;
+                    if (xr >= BH) {
+                        xr -= BH;
+                        ++xs;
+                    }
                     const float4* src = reinterpret_cast<const float4*>(produ + r * BWU + sidx * G::SPU);
                     float o[G::SPU];
                     float4 q4;
@@ -256,8 +271,16 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                         dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
                 }
             } else {
-                for (int jt = tid - NA / 2; jt < G::XITEMS - G::XU_ITEMS; jt += NA / 2) {
-                    const int r = jt % BH, sidx = (jt / BH) % G::NSP, c = jt / (BH * G::NSP);
+                const int j0 = tid - NA / 2;
+                int xr = j0 % BH, xs = j0 / BH;  // (row, strip + NSP * channel)
+                for (int jt = j0; jt < G::XITEMS - G::XU_ITEMS; jt += NA / 2) {
+                    const int r = xr, sidx = xs % G::NSP, c = xs / G::NSP;
+                    xr += (NA / 2) % BH;
+                    xs += (NA / 2) / BH;
+                    if (xr >= BH) {
+                        xr -= BH;
+                        ++xs;
+                    }
                     const float4* src = reinterpret_cast<const float4*>(
                         prodp + c * PBP + r * BWP + 2 * sidx * G::SPP);
                     float2 o[G::SPP];
@@ -293,10 +316,13 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         // =====================================================================
         setmaxnreg_inc<G::RB>();
         const int bt = tid - NA;
-        const int band = bt >> 4;         // rows 4*band .. 4*band+3 of the tile
-        const int cp = bt & 15;           // columns 2cp, 2cp+1
-        const int bwarp = bt >> 5;
+        const int band = bt >> 4;  // rows 4*band .. 4*band+3 of the tile
+        const int cp = bt & 15;    // columns 2cp, 2cp+1
+        const int lane = bt & 31;
         const float inv_alpha = a.inv_alpha;
+        const bool first = a.first_group, last = a.last_group;
+        const long long plane_stride = static_cast<long long>(a.H) * a.pitch;
+        const int pitch = a.pitch;
 
         float2 ringu[4][K];          // (col 2cp, col 2cp+1) of u
         float2 ringp[CG][4][2][K];   // (F u, F^2 u) per column
@@ -314,20 +340,34 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
-        int cnt = 0, slot = 0, outc = 0;
-        for (; !q.done; q.next()) {
+        int cnt = 0;
+        // per-segment geometry (recomputed when the schedule moves to a new tile)
+        int seg = -1, rows = 0, gband = 0, half = 0;
+        bool x1in = false;
+        long long col_off = 0;
+
+        // one plane with ring slot S_; the caller unrolls K planes so every
+        // ring index is a compile-time constant (no rotation moves)
+        auto plane = [&](auto slot_c) {
+            constexpr int S_ = decltype(slot_c)::value;
+            if (q.i != seg) {
+                seg = q.i;
+                const int y0 = q.tile_y * TY + band * 4;
+                const int x0 = q.tile_x * TX + 2 * cp;
+                rows = x0 < a.W ? max(0, min(4, a.H - y0)) : 0;
+                x1in = x0 + 1 < a.W;
+                col_off = static_cast<long long>(y0) * pitch + x0;
+                gband = q.tile_y * G::NBANDS + band;
+                half = q.tile_x;
+            }
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const int out_p = q.p - RT;
             const bool emit = out_p >= q.ta;
             const int to = a.out_t0 + out_p;
-            const int y0 = q.tile_y * TY + band * 4;
-            const int x0 = q.tile_x * TX + 2 * cp;
-            const int rows = x0 < a.W ? min(4, a.H - y0) : 0;
-            const long long col_off = static_cast<long long>(y0) * a.pitch + x0;
-            // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending)
-            float2 yu[4];
-            float2 yp[CG][4][2];
+
+            // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending),
+            // accumulated straight into this plane's ring slot
             if (valid) {
                 const int b = cnt & 1;
                 mbar_wait(&xb_full[b], (cnt >> 1) & 1);
@@ -341,28 +381,30 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     for (int r = 0; r < 4; ++r) {
                         const int d = j - r;
                         if (d < 0 || d > 2 * R) continue;
-                        yu[r] = d == 0 ? A::mul2(a.taps_y[0], vin, zero2)
-                                       : A::mac2(yu[r], a.taps_y[d], vin, one2, zero2);
+                        ringu[r][S_] = d == 0 ? A::mul2(a.taps_y[0], vin, zero2)
+                                              : A::mac2(ringu[r][S_], a.taps_y[d], vin, one2, zero2);
                     }
                 }
 #pragma unroll
                 for (int c = 0; c < CG; ++c) {
-                    const float4* sp4 =
+                    const float4* sq =
                         reinterpret_cast<const float4*>(xbp + c * XBP + (band * 4) * TXQ) + cp;
 #pragma unroll
                     for (int j = 0; j < 4 + 2 * R; ++j) {
-                        const float4 v4 = sp4[j * (TXQ / 4)];
+                        const float4 v4 = sq[j * (TXQ / 4)];
                         const float2 v0 = make_float2(v4.x, v4.y), v1 = make_float2(v4.z, v4.w);
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             const int d = j - r;
                             if (d < 0 || d > 2 * R) continue;
                             if (d == 0) {
-                                yp[c][r][0] = A::mul2(a.taps_y[0], v0, zero2);
-                                yp[c][r][1] = A::mul2(a.taps_y[0], v1, zero2);
+                                ringp[c][r][0][S_] = A::mul2(a.taps_y[0], v0, zero2);
+                                ringp[c][r][1][S_] = A::mul2(a.taps_y[0], v1, zero2);
                             } else {
-                                yp[c][r][0] = A::mac2(yp[c][r][0], a.taps_y[d], v0, one2, zero2);
-                                yp[c][r][1] = A::mac2(yp[c][r][1], a.taps_y[d], v1, one2, zero2);
+                                ringp[c][r][0][S_] =
+                                    A::mac2(ringp[c][r][0][S_], a.taps_y[d], v0, one2, zero2);
+                                ringp[c][r][1][S_] =
+                                    A::mac2(ringp[c][r][1][S_], a.taps_y[d], v1, one2, zero2);
                             }
                         }
                     }
@@ -372,109 +414,95 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             } else {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    yu[r] = make_float2(0.0f, 0.0f);
+                    ringu[r][S_] = make_float2(0.0f, 0.0f);
 #pragma unroll
-                    for (int c = 0; c < CG; ++c) yp[c][r][0] = yp[c][r][1] = make_float2(0.0f, 0.0f);
+                    for (int c = 0; c < CG; ++c)
+                        ringp[c][r][0][S_] = ringp[c][r][1][S_] = make_float2(0.0f, 0.0f);
                 }
             }
-            // S^p and F_c of the output plane (L2-resident: loaded by TMA RT
-            // planes ago); issued here, consumed in the epilogue
-            float2 spv[4], fv[CG][4];
             if (emit) {
-                const long long plane = static_cast<long long>(to - a.buf_t0) * a.H * a.pitch;
-                const float* ps = a.sp + plane + col_off;
+                // S^p and F_c of the output plane (L2-resident: TMA loaded them
+                // RT planes ago)
+                const long long pbase = static_cast<long long>(to - a.buf_t0) * plane_stride + col_off;
+                float2 spv[4], fv[CG][4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(ps + r * a.pitch))
+                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.sp + pbase + r * pitch))
                                       : make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int c = 0; c < CG; ++c)
-                        fv[c][r] = r < rows
-                                       ? __ldg(reinterpret_cast<const float2*>(a.f[c] + plane + col_off + r * a.pitch))
-                                       : make_float2(0.0f, 0.0f);
+                        fv[c][r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.f[c] + pbase + r * pitch))
+                                            : make_float2(0.0f, 0.0f);
                 }
-            }
-            // t-pass (conv3d.cpp:147-165) out of the ring, row by row, each row
-            // recombined and stored at once (keeps few values live); planes
-            // oldest..newest take taps_t[0..2RT]; a switch on the slot keeps
-            // the ring indices static
-            const bool first = a.first_group;
-            float* orow = a.out + static_cast<long long>(to - a.out_buf_t0) * a.H * a.pitch + col_off;
-            double cs0 = 0.0, cs1 = 0.0;
-            float cmax = 0.0f;
-            auto t_step = [&](auto slot_c) {
-                constexpr int S_ = decltype(slot_c)::value;
+                float* orow = a.out + static_cast<long long>(to - a.out_buf_t0) * plane_stride + col_off;
+                double cs0 = 0.0, cs1 = 0.0;
+                float cmax = 0.0f;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    ringu[r][S_] = yu[r];
+                    // t-pass (conv3d.cpp:147-165): planes oldest..newest take
+                    // taps_t[0..2RT]; first = w * in, then +=
                     float2 zu = A::mul2(a.taps_t[0], ringu[r][(S_ + 1) % K], zero2);
 #pragma unroll
                     for (int d = 1; d < K; ++d)
                         zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % K], one2, zero2);
-                    float2 zp[CG][2];
+                    float2 prev = make_float2(0.0f, 0.0f);
+                    if (!first && r < rows) prev = *reinterpret_cast<const float2*>(orow + r * pitch);
+                    float v[2] = {0.0f, 0.0f};
 #pragma unroll
                     for (int c = 0; c < CG; ++c)
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
-                            ringp[c][r][j][S_] = yp[c][r][j];
-                            float2 acp = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % K], zero2);
+                            float2 z = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % K], zero2);
 #pragma unroll
                             for (int d = 1; d < K; ++d)
-                                acp = A::mac2(acp, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % K],
-                                              one2, zero2);
-                            zp[c][j] = acp;
+                                z = A::mac2(z, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % K], one2, zero2);
+                            // engine.cpp:113-119, channel sum engine.cpp:157-162
+                            const float term = A::recombine(j ? spv[r].y : spv[r].x,
+                                                            j ? fv[c][r].y : fv[c][r].x, inv_alpha,
+                                                            j ? zu.y : zu.x, z.y, z.x);
+                            v[j] = c > 0 ? xadd(v[j], term)
+                                         : (first ? term : xadd(j ? prev.y : prev.x, term));
                         }
-                    if (!emit) continue;
-                    // recombination + channel sum (engine.cpp:113-119, 157-162), store
-                    float2 prev = make_float2(0.0f, 0.0f);
-                    if (!first && r < rows) prev = *reinterpret_cast<const float2*>(orow + r * a.pitch);
-                    float v[2];
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const float Au = j ? zu.y : zu.x;
-                        const float sp_ = j ? spv[r].y : spv[r].x;
-                        float acc = 0.0f;
-#pragma unroll
-                        for (int c = 0; c < CG; ++c) {
-                            const float f_ = j ? fv[c][r].y : fv[c][r].x;
-                            const float term =
-                                A::recombine(sp_, f_, inv_alpha, Au, zp[c][j].y, zp[c][j].x);
-                            acc = c > 0 ? xadd(acc, term)
-                                        : (first ? term : xadd(j ? prev.y : prev.x, term));
-                        }
-                        v[j] = acc;
-                    }
-                    if (r < rows) *reinterpret_cast<float2*>(orow + r * a.pitch) = make_float2(v[0], v[1]);
+                    if (r < rows) *reinterpret_cast<float2*>(orow + r * pitch) = make_float2(v[0], v[1]);
                     // only points inside the volume enter the reductions
                     const float v0 = r < rows ? v[0] : 0.0f;
-                    const float v1 = (r < rows && x0 + 1 < a.W) ? v[1] : 0.0f;
+                    const float v1 = (r < rows && x1in) ? v[1] : 0.0f;
                     cs0 += static_cast<double>(v0) * static_cast<double>(v0);
                     cs1 += static_cast<double>(v1) * static_cast<double>(v1);
                     cmax = fmaxf(cmax, fmaxf(v0, v1));
                 }
-            };
-            SFK_RING_SWITCH(slot, t_step)
-            slot = (slot + 1 == K) ? 0 : slot + 1;
-            if (!emit) continue;
-            if (a.last_group) {
-                // canonical reduction (device_common.cuh), warp-local: a warp
-                // holds two whole bands (lanes 0-15 band 2w, 16-31 band 2w+1),
-                // lane l of a half holds columns 2l and 2l+1. The 32-column
-                // butterfly (16, 8, 4, 2, 1) becomes xor 8, 4, 2, 1 over the
-                // half-warp plus the final even+odd add inside the lane.
+                if (last) {
+                    // canonical reduction (device_common.cuh), warp-local: a warp
+                    // holds two whole bands (lanes 0-15 band 2w, 16-31 band 2w+1),
+                    // lane l of a half holds columns 2l and 2l+1. The 32-column
+                    // butterfly (16, 8, 4, 2, 1) becomes xor 8, 4, 2, 1 over the
+                    // half-warp plus the final even+odd add inside the lane.
 #pragma unroll
-                for (int o = 8; o >= 1; o >>= 1) {
-                    cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
-                    cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
+                    for (int o = 8; o >= 1; o >>= 1) {
+                        cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
+                        cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
+                    }
+                    const double sum = cs0 + cs1;
+                    const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                    if ((lane & 15) == 0 && gband < a.nbands && half < a.nhalves)
+                        a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gband) * a.nhalves +
+                               half] = sum;
+                    if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
                 }
-                const double s = cs0 + cs1;
-                const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
-                const int lane = bt & 31;
-                const int gband = q.tile_y * G::NBANDS + band;
-                if ((lane & 15) == 0 && gband < a.nbands && q.tile_x < a.nhalves)
-                    a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gband) * a.nhalves + q.tile_x] = s;
-                if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
             }
+            q.next();
+        };
+        using std::integral_constant;
+        while (!q.done) {
+            plane(integral_constant<int, 0>{});
+            if constexpr (K > 1) { if (q.done) break; plane(integral_constant<int, (K > 1 ? 1 : 0)>{}); }
+            if constexpr (K > 2) { if (q.done) break; plane(integral_constant<int, (K > 2 ? 2 : 0)>{}); }
+            if constexpr (K > 3) { if (q.done) break; plane(integral_constant<int, (K > 3 ? 3 : 0)>{}); }
+            if constexpr (K > 4) { if (q.done) break; plane(integral_constant<int, (K > 4 ? 4 : 0)>{}); }
+            if constexpr (K > 5) { if (q.done) break; plane(integral_constant<int, (K > 5 ? 5 : 0)>{}); }
+            if constexpr (K > 6) { if (q.done) break; plane(integral_constant<int, (K > 6 ? 6 : 0)>{}); }
+            if constexpr (K > 7) { if (q.done) break; plane(integral_constant<int, (K > 7 ? 7 : 0)>{}); }
+            if constexpr (K > 8) { if (q.done) break; plane(integral_constant<int, (K > 8 ? 8 : 0)>{}); }
         }
     }
 }
