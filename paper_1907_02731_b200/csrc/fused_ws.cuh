@@ -59,17 +59,22 @@ struct WsGeom {
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;
     static constexpr int XBP = (BH * TXQ + 31) / 32 * 32;
     static constexpr int XBUF = XBU + CG * XBP;  // one x-pass buffer
-    static constexpr int SPU = 4, SPP = 4;  // 2 x 8 x BH strips: even split over A
+    static constexpr int SPU = 4, SPP = 4;  // 8 u strips and 8 pair strips of 4 columns
     static constexpr int NSU = TX / SPU, NSP = TX / SPP;
-    static constexpr int XU_ITEMS = NSU * BH, XITEMS = XU_ITEMS + CG * NSP * BH;
     static constexpr int NINU = SPU + 2 * R, NINP = SPP + 2 * R;
     static constexpr int NBANDS = TY / 4;
+    // products: thread -> (row lane, float4 column); NPR rows per pass
+    static constexpr int NPR = NA / BW4, PPASS = (BH + NPR - 1) / NPR;
+    // x-pass: half the A threads take the u strips, half the pair strips;
+    // in a half, thread -> (strip, row lane); RL rows per pass
+    static constexpr int NH = NA / 2, RL = NH / NSU, XPASS = (BH + RL - 1) / RL;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
     static constexpr size_t PROD_FLOATS = size_t(PBU) + size_t(CG) * PBP;
     static constexpr size_t XB_FLOATS = 2 * size_t(XBUF);
-    static constexpr size_t RED_FLOATS = 2 * (2 * NBANDS * 32) + 2 * 16;  // doubles + warp max
+    static constexpr size_t OT_FLOATS = 2 * size_t(TY) * TX;  // double-buffered output tile
     static constexpr size_t SMEM_BYTES =
-        (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + RED_FLOATS) * sizeof(float) + 128;
+        (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + OT_FLOATS) * sizeof(float) + 128;
+    static_assert(NSU == NSP && NH % NSU == 0 && RL % 8 == 0, "x-pass thread mapping");
     static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
     static_assert(CG == 1 || true, "pair strips are split over the second half of A");
     static_assert(NA * RA + NB * RB <= NT * RPOOL, "register pool of the CTA");
@@ -94,9 +99,8 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
     float* produ = raw + G::RAW_FLOATS;     // [BH][BWU]           u
     float* prodp = produ + PBU;             // [CG][BH][BWP]       (F u, F^2 u)
     float* xb = prodp + CG * PBP;           // [2][XBUF]           x-pass output
-    double* red = reinterpret_cast<double*>(xb + G::XB_FLOATS);  // [2][NBANDS][32]
-    float* redmax = reinterpret_cast<float*>(red + 2 * G::NBANDS * 32);  // [2][8]
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(redmax + 2 * 16);
+    float* otile = xb + G::XB_FLOATS;       // [2][TY][TX]         output tiles (TMA store)
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(otile + G::OT_FLOATS);
     uint64_t* raw_full = mbar;             // [STAGES]  TMA -> A
     uint64_t* xb_full = mbar + STAGES;     // [2]       A -> B (count NA)
     uint64_t* xb_empty = mbar + STAGES + 2;  // [2]     B -> A (count NB)
@@ -162,6 +166,11 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         const double inv = st.mode == 0 ? 1.0 : st.inv;  // float(double(y)*1.0) == y
         const float inv_f = st.mode == 0 ? 1.0f : st.inv_f;
 
+        const int pr0 = tid / BW4, pc4 = tid - (tid / BW4) * BW4;
+        const bool pact = tid < G::NPR * BW4;
+        const int xh = tid / G::NH, xt = tid - xh * G::NH;
+        const int xs = xt / G::RL, xr0 = xt - xs * G::RL;
+
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
         int cnt = 0;  // in-volume planes handled
@@ -171,59 +180,63 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             const int s = cnt % STAGES;
             mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
             const float* rs = raw + static_cast<size_t>(s) * NIN * FB;
-            // products over the halo box (engine.cpp:92-100), 4 points per item
-            // items i = tid, tid+NA, ...: (row, float4 column) advanced incrementally
-            int pr = tid / BW4, pc4 = tid - (tid / BW4) * BW4;
-            for (int i = tid; i < BH * BW4; i += NA) {
-                const int r = pr, c4 = pc4;
-                pr += NA / BW4;
-                pc4 += NA % BW4;
-                if (pc4 >= BW4) {
-                    pc4 -= BW4;
-                    ++pr;
-                }
-                const float4 yv = reinterpret_cast<const float4*>(rs)[i];
-                const float4 sv = reinterpret_cast<const float4*>(rs + FB)[i];
-                float4 xv;
-                if (sigm) {
-                    xv.x = A::load_sigmoid(yv.x, st);
-                    xv.y = A::load_sigmoid(yv.y, st);
-                    xv.z = A::load_sigmoid(yv.z, st);
-                    xv.w = A::load_sigmoid(yv.w, st);
-                } else {
-                    xv.x = A::load_norm(yv.x, inv, inv_f);
-                    xv.y = A::load_norm(yv.y, inv, inv_f);
-                    xv.z = A::load_norm(yv.z, inv, inv_f);
-                    xv.w = A::load_norm(yv.w, inv, inv_f);
-                }
-                float4 u;
-                u.x = A::mul(sv.x, xv.x);
-                u.y = A::mul(sv.y, xv.y);
-                u.z = A::mul(sv.z, xv.z);
-                u.w = A::mul(sv.w, xv.w);
-                *reinterpret_cast<float4*>(produ + r * BWU + 4 * c4) = u;
-#pragma unroll
-                for (int cg = 0; cg < CG; ++cg) {
-                    const float4 fv = reinterpret_cast<const float4*>(rs + (2 + cg) * FB)[i];
-                    float4 p0, p1;  // (F S^p X, (F F) S^p X) per point
-                    p0.x = A::mul(fv.x, u.x);
-                    p0.z = A::mul(fv.y, u.y);
-                    p1.x = A::mul(fv.z, u.z);
-                    p1.z = A::mul(fv.w, u.w);
-                    if constexpr (FMA) {  // FAST: F (F u), one product less
-                        p0.y = fv.x * p0.x;
-                        p0.w = fv.y * p0.z;
-                        p1.y = fv.z * p1.x;
-                        p1.w = fv.w * p1.z;
-                    } else {  // engine.cpp:98: fi * fi * sx
-                        p0.y = A::mul(A::mul(fv.x, fv.x), u.x);
-                        p0.w = A::mul(A::mul(fv.y, fv.y), u.y);
-                        p1.y = A::mul(A::mul(fv.z, fv.z), u.z);
-                        p1.w = A::mul(A::mul(fv.w, fv.w), u.w);
+            // products over the halo box (engine.cpp:92-100): thread -> (row
+            // lane pr0, float4 column pc4), rows pr0, pr0 + NPR, ... (constant
+            // offsets, no index arithmetic in the loop)
+            if (pact) {
+                const float4* rx = reinterpret_cast<const float4*>(rs) + pr0 * BW4 + pc4;
+                float* du = produ + pr0 * BWU + 4 * pc4;
+                float* dp = prodp + pr0 * BWP + 8 * pc4;
+                // EXACT's double-precision load_norm needs more registers than
+                // A's budget allows for an unrolled loop
+                constexpr int PU = FMA ? G::PPASS : 1;
+#pragma unroll PU
+                for (int k = 0; k < G::PPASS; ++k) {
+                    if (k == G::PPASS - 1 && pr0 + k * G::NPR >= BH) break;
+                    const int i = k * G::NPR * BW4;
+                    const float4 yv = rx[i];
+                    const float4 sv = rx[FB / 4 + i];
+                    float4 xv;
+                    if (sigm) {
+                        xv.x = A::load_sigmoid(yv.x, st);
+                        xv.y = A::load_sigmoid(yv.y, st);
+                        xv.z = A::load_sigmoid(yv.z, st);
+                        xv.w = A::load_sigmoid(yv.w, st);
+                    } else {
+                        xv.x = A::load_norm(yv.x, inv, inv_f);
+                        xv.y = A::load_norm(yv.y, inv, inv_f);
+                        xv.z = A::load_norm(yv.z, inv, inv_f);
+                        xv.w = A::load_norm(yv.w, inv, inv_f);
                     }
-                    float4* pp = reinterpret_cast<float4*>(prodp + cg * PBP + r * BWP + 8 * c4);
-                    pp[0] = p0;
-                    pp[1] = p1;
+                    float4 u;
+                    u.x = A::mul(sv.x, xv.x);
+                    u.y = A::mul(sv.y, xv.y);
+                    u.z = A::mul(sv.z, xv.z);
+                    u.w = A::mul(sv.w, xv.w);
+                    *reinterpret_cast<float4*>(du + k * G::NPR * BWU) = u;
+#pragma unroll
+                    for (int cg = 0; cg < CG; ++cg) {
+                        const float4 fv = rx[(2 + cg) * (FB / 4) + i];
+                        float4 p0, p1;  // (F S^p X, (F F) S^p X) per point
+                        p0.x = A::mul(fv.x, u.x);
+                        p0.z = A::mul(fv.y, u.y);
+                        p1.x = A::mul(fv.z, u.z);
+                        p1.z = A::mul(fv.w, u.w);
+                        if constexpr (FMA) {  // FAST: F (F u), one product less
+                            p0.y = fv.x * p0.x;
+                            p0.w = fv.y * p0.z;
+                            p1.y = fv.z * p1.x;
+                            p1.w = fv.w * p1.z;
+                        } else {  // engine.cpp:98: fi * fi * sx
+                            p0.y = A::mul(A::mul(fv.x, fv.x), u.x);
+                            p0.w = A::mul(A::mul(fv.y, fv.y), u.y);
+                            p1.y = A::mul(A::mul(fv.z, fv.z), u.z);
+                            p1.w = A::mul(A::mul(fv.w, fv.w), u.w);
+                        }
+                        float4* pp = reinterpret_cast<float4*>(dp + cg * PBP + k * G::NPR * BWP);
+                        pp[0] = p0;
+                        pp[1] = p1;
+                    }
                 }
             }
             named_bar_sync(1, NA);  // products ready; raw stage s fully read
@@ -236,19 +249,14 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
-            // the first NA/2 threads take the u strips, the others the pair
-            // strips (equal counts and costs); lanes take consecutive rows
-            if (tid < NA / 2) {
-                int xr = tid % BH, xs = tid / BH;  // strip (row, index), advanced incrementally
-                for (int it = tid; it < G::XU_ITEMS; it += NA / 2) {
-                    const int r = xr, sidx = xs;
-                    xr += (NA / 2) % BH;
-                    xs += (NA / 2) / BH;
-                    if (xr >= BH) {
-                        xr -= BH;
-                        ++xs;
-                    }
-                    const float4* src = reinterpret_cast<const float4*>(produ + r * BWU + sidx * G::SPU);
+            if (xh == 0) {
+                // u strips: rows xr0, xr0 + RL, ... of strip xs
+                const float* srcb = produ + xr0 * BWU + xs * G::SPU;
+                float* dstb = xbu + xr0 * TXU + xs * G::SPU;
+#pragma unroll
+                for (int k = 0; k < G::XPASS; ++k) {
+                    if (k == G::XPASS - 1 && xr0 + k * G::RL >= BH) break;
+                    const float4* src = reinterpret_cast<const float4*>(srcb + k * G::RL * BWU);
                     float o[G::SPU];
                     float4 q4;
 #pragma unroll
@@ -265,45 +273,39 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                             o[j] = d == 0 ? A::mul(a.taps_x[0], vin) : A::mac(o[j], a.taps_x[d], vin);
                         }
                     }
-                    float4* dst = reinterpret_cast<float4*>(xbu + r * TXU + sidx * G::SPU);
-#pragma unroll
-                    for (int v = 0; v < G::SPU / 4; ++v)
-                        dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+                    *reinterpret_cast<float4*>(dstb + k * G::RL * TXU) = make_float4(o[0], o[1], o[2], o[3]);
                 }
             } else {
-                const int j0 = tid - NA / 2;
-                int xr = j0 % BH, xs = j0 / BH;  // (row, strip + NSP * channel)
-                for (int jt = j0; jt < G::XITEMS - G::XU_ITEMS; jt += NA / 2) {
-                    const int r = xr, sidx = xs % G::NSP, c = xs / G::NSP;
-                    xr += (NA / 2) % BH;
-                    xs += (NA / 2) / BH;
-                    if (xr >= BH) {
-                        xr -= BH;
-                        ++xs;
-                    }
-                    const float4* src = reinterpret_cast<const float4*>(
-                        prodp + c * PBP + r * BWP + 2 * sidx * G::SPP);
-                    float2 o[G::SPP];
-                    float4 q4;
 #pragma unroll
-                    for (int m2 = 0; m2 < (G::XOFF + G::NINP + 1) / 2 * 2; ++m2) {
-                        if (m2 % 2 == 0) q4 = src[m2 / 2];
-                        const int m = m2 - G::XOFF;
-                        if (m < 0 || m >= G::NINP) continue;
-                        const float2 vin = (m2 % 2 == 0) ? make_float2(q4.x, q4.y)
-                                                         : make_float2(q4.z, q4.w);
+                for (int c = 0; c < CG; ++c) {
+                    const float* srcb = prodp + c * PBP + xr0 * BWP + 2 * xs * G::SPP;
+                    float* dstb = xbp + c * XBP + xr0 * TXQ + 2 * xs * G::SPP;
 #pragma unroll
-                        for (int j = 0; j < G::SPP; ++j) {
-                            const int d = m - j;
-                            if (d < 0 || d > 2 * R) continue;
-                            o[j] = d == 0 ? A::mul2(a.taps_x[0], vin, zero2)
-                                          : A::mac2(o[j], a.taps_x[d], vin, one2, zero2);
+                    for (int k = 0; k < G::XPASS; ++k) {
+                        if (k == G::XPASS - 1 && xr0 + k * G::RL >= BH) break;
+                        const float4* src = reinterpret_cast<const float4*>(srcb + k * G::RL * BWP);
+                        float2 o[G::SPP];
+                        float4 q4;
+#pragma unroll
+                        for (int m2 = 0; m2 < (G::XOFF + G::NINP + 1) / 2 * 2; ++m2) {
+                            if (m2 % 2 == 0) q4 = src[m2 / 2];
+                            const int m = m2 - G::XOFF;
+                            if (m < 0 || m >= G::NINP) continue;
+                            const float2 vin = (m2 % 2 == 0) ? make_float2(q4.x, q4.y)
+                                                             : make_float2(q4.z, q4.w);
+#pragma unroll
+                            for (int j = 0; j < G::SPP; ++j) {
+                                const int d = m - j;
+                                if (d < 0 || d > 2 * R) continue;
+                                o[j] = d == 0 ? A::mul2(a.taps_x[0], vin, zero2)
+                                              : A::mac2(o[j], a.taps_x[d], vin, one2, zero2);
+                            }
                         }
-                    }
-                    float4* dst = reinterpret_cast<float4*>(xbp + c * XBP + r * TXQ + 2 * sidx * G::SPP);
+                        // float2 stores straight from the FFMA2 register pairs
+                        float2* dst = reinterpret_cast<float2*>(dstb + k * G::RL * TXQ);
 #pragma unroll
-                    for (int v = 0; v < G::SPP / 2; ++v)
-                        dst[v] = make_float4(o[2 * v].x, o[2 * v].y, o[2 * v + 1].x, o[2 * v + 1].y);
+                        for (int j = 0; j < G::SPP; ++j) dst[j] = o[j];
+                    }
                 }
             }
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
@@ -340,11 +342,15 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
-        int cnt = 0;
-        // per-segment geometry (recomputed when the schedule moves to a new tile)
-        int seg = -1, rows = 0, gband = 0, half = 0;
-        bool x1in = false;
-        long long col_off = 0;
+        int cnt = 0;   // in-volume planes consumed
+        int ecnt = 0;  // output planes emitted (selects the output tile)
+        // per-segment geometry (recomputed when the schedule moves to a new
+        // tile): element offsets of this thread's 4 rows inside a plane (rows
+        // past H are clamped so every load stays inside the buffer; their
+        // results are clipped by the TMA store and masked out of the sums)
+        int seg = -1, gband = 0, half = 0;
+        int roff[4];
+        bool rok[4], c1ok = false;
 
         // one plane with ring slot S_; the caller unrolls K planes so every
         // ring index is a compile-time constant (no rotation moves)
@@ -354,9 +360,12 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 seg = q.i;
                 const int y0 = q.tile_y * TY + band * 4;
                 const int x0 = q.tile_x * TX + 2 * cp;
-                rows = x0 < a.W ? max(0, min(4, a.H - y0)) : 0;
-                x1in = x0 + 1 < a.W;
-                col_off = static_cast<long long>(y0) * pitch + x0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    rok[r] = y0 + r < a.H && x0 < a.W;
+                    roff[r] = min(y0 + r, a.H - 1) * pitch + x0;
+                }
+                c1ok = x0 + 1 < a.W;
                 gband = q.tile_y * G::NBANDS + band;
                 half = q.tile_x;
             }
@@ -365,6 +374,24 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             const int out_p = q.p - RT;
             const bool emit = out_p >= q.ta;
             const int to = a.out_t0 + out_p;
+
+            // S^p and F_c of the output plane: pulled from L2 into L1 before the
+            // y-pass (TMA brought them in RT planes ago), read after it; holding
+            // them in registers across the y-pass would spill the ring
+            const float* spp = nullptr;
+            const float* fpp[CG];
+            if (emit) {
+                const long long po = static_cast<long long>(to - a.buf_t0) * plane_stride;
+                spp = a.sp + po;
+#pragma unroll
+                for (int c = 0; c < CG; ++c) fpp[c] = a.f[c] + po;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    prefetch_l1(spp + roff[r]);
+#pragma unroll
+                    for (int c = 0; c < CG; ++c) prefetch_l1(fpp[c] + roff[r]);
+                }
+            }
 
             // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending),
             // accumulated straight into this plane's ring slot
@@ -421,20 +448,20 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 }
             }
             if (emit) {
-                // S^p and F_c of the output plane (L2-resident: TMA loaded them
-                // RT planes ago)
-                const long long pbase = static_cast<long long>(to - a.buf_t0) * plane_stride + col_off;
                 float2 spv[4], fv[CG][4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    spv[r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.sp + pbase + r * pitch))
-                                      : make_float2(0.0f, 0.0f);
+                    spv[r] = __ldg(reinterpret_cast<const float2*>(spp + roff[r]));
 #pragma unroll
-                    for (int c = 0; c < CG; ++c)
-                        fv[c][r] = r < rows ? __ldg(reinterpret_cast<const float2*>(a.f[c] + pbase + r * pitch))
-                                            : make_float2(0.0f, 0.0f);
+                    for (int c = 0; c < CG; ++c) fv[c][r] = __ldg(reinterpret_cast<const float2*>(fpp[c] + roff[r]));
                 }
-                float* orow = a.out + static_cast<long long>(to - a.out_buf_t0) * plane_stride + col_off;
+                float2 prev[4];
+                if (!first) {  // channel groups after the first add to y_{k+1}
+                    const float* op = a.out + static_cast<long long>(to - a.out_buf_t0) * plane_stride;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) prev[r] = *reinterpret_cast<const float2*>(op + roff[r]);
+                }
+                float* ot = otile + (ecnt & 1) * (TY * TX) + (band * 4) * TX + 2 * cp;
                 double cs0 = 0.0, cs1 = 0.0;
                 float cmax = 0.0f;
 #pragma unroll
@@ -445,8 +472,6 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
 #pragma unroll
                     for (int d = 1; d < K; ++d)
                         zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % K], one2, zero2);
-                    float2 prev = make_float2(0.0f, 0.0f);
-                    if (!first && r < rows) prev = *reinterpret_cast<const float2*>(orow + r * pitch);
                     float v[2] = {0.0f, 0.0f};
 #pragma unroll
                     for (int c = 0; c < CG; ++c)
@@ -461,16 +486,29 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                                                             j ? fv[c][r].y : fv[c][r].x, inv_alpha,
                                                             j ? zu.y : zu.x, z.y, z.x);
                             v[j] = c > 0 ? xadd(v[j], term)
-                                         : (first ? term : xadd(j ? prev.y : prev.x, term));
+                                         : (first ? term : xadd(j ? prev[r].y : prev[r].x, term));
                         }
-                    if (r < rows) *reinterpret_cast<float2*>(orow + r * pitch) = make_float2(v[0], v[1]);
+                    *reinterpret_cast<float2*>(ot + r * TX) = make_float2(v[0], v[1]);
                     // only points inside the volume enter the reductions
-                    const float v0 = r < rows ? v[0] : 0.0f;
-                    const float v1 = (r < rows && x1in) ? v[1] : 0.0f;
+                    const float v0 = rok[r] ? v[0] : 0.0f;
+                    const float v1 = (rok[r] && c1ok) ? v[1] : 0.0f;
                     cs0 += static_cast<double>(v0) * static_cast<double>(v0);
                     cs1 += static_cast<double>(v1) * static_cast<double>(v1);
                     cmax = fmaxf(cmax, fmaxf(v0, v1));
                 }
+                // hand the tile to the TMA unit: generic-proxy writes -> async
+                // proxy, then one thread stores it (clipped at the volume edge).
+                // The store of tile e-2 (same buffer) was drained by the
+                // wait_group.read before the barrier of plane e-1.
+                fence_proxy_async();
+                if (bt == 0) bulk_wait_read0();
+                named_bar_sync(2, NB);
+                if (bt == 0) {
+                    tma_store_3d(&a.tm_out, otile + (ecnt & 1) * (TY * TX), q.tile_x * TX, q.tile_y * TY,
+                                 to - a.out_buf_t0);
+                    bulk_commit();
+                }
+                ++ecnt;
                 if (last) {
                     // canonical reduction (device_common.cuh), warp-local: a warp
                     // holds two whole bands (lanes 0-15 band 2w, 16-31 band 2w+1),
@@ -504,6 +542,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             if constexpr (K > 7) { if (q.done) break; plane(integral_constant<int, (K > 7 ? 7 : 0)>{}); }
             if constexpr (K > 8) { if (q.done) break; plane(integral_constant<int, (K > 8 ? 8 : 0)>{}); }
         }
+        if (bt == 0) bulk_wait0();  // the output tiles are read before the CTA exits
     }
 }
 

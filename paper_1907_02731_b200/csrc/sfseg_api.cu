@@ -566,6 +566,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         std::memset(&a, 0, sizeof a);
         a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
         a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+        a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, v->ty);
         a.sp = c->sp;
         a.out = out;
         a.part = c->part;

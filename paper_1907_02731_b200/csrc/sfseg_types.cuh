@@ -29,6 +29,7 @@ struct FusedArgs {
     CUtensorMap tm_x;           // iterate source y_k (or S / x0 at iteration 1)
     CUtensorMap tm_sp;          // S^p
     CUtensorMap tm_f[kMaxCG];   // feature channels of this group
+    CUtensorMap tm_out;         // y_{k+1}, box = one output tile (TMA store)
     const float* sp;            // pitched S^p (recombination reload)
     const float* f[kMaxCG];
     float* out;                 // pitched y_{k+1}
