@@ -33,6 +33,12 @@
 #include "fused_step.cuh"  // PlaneStream, Arith, canonical_tree32, SFK_RING_SWITCH
 #include "sfseg_types.cuh"
 
+// ablation builds (tools/ablate.sh): bit 0 drops A's arithmetic, bit 1 B's;
+// the pipeline (TMA, barriers, stores) still runs. Never set in the product.
+#ifndef SFK_EXP
+#define SFK_EXP 0
+#endif
+
 namespace sfk {
 
 template <int RT, int R, int CG, int STAGES, int NWA = 8>
@@ -69,11 +75,16 @@ struct WsGeom {
     // in a half, thread -> (strip, row lane); RL rows per pass
     static constexpr int NH = NA / 2, RL = NH / NSU, XPASS = (BH + RL - 1) / RL;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
-    static constexpr size_t PROD_FLOATS = size_t(PBU) + size_t(CG) * PBP;
-    static constexpr size_t XB_FLOATS = 2 * size_t(XBUF);
-    static constexpr size_t OT_FLOATS = 2 * size_t(TY) * TX;  // double-buffered output tile
+    // (SFK_EXP bit 3, skeleton ablations only: no product / x-pass storage)
+    static constexpr size_t PROD_FLOATS = (SFK_EXP & 8) ? 32 : size_t(PBU) + size_t(CG) * PBP;
+    static constexpr size_t XB_FLOATS = (SFK_EXP & 8) ? 64 : 2 * size_t(XBUF);
+    // per B warp, double-buffered: S^p and F_c of its 8 output rows, TMA-loaded
+    // a plane ahead; the S^p slab is overwritten with y_{k+1} and TMA-stored
+    static constexpr int SLAB = 8 * TX;
+    static constexpr int NSF = 1 + CG;  // slab fields: S^p, F_c...
+    static constexpr size_t IN_FLOATS = size_t(NB / 32) * 2 * NSF * SLAB;
     static constexpr size_t SMEM_BYTES =
-        (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + OT_FLOATS) * sizeof(float) + 128;
+        (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + IN_FLOATS) * sizeof(float) + 256;
     static_assert(NSU == NSP && NH % NSU == 0 && RL % 8 == 0, "x-pass thread mapping");
     static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
     static_assert(CG == 1 || true, "pair strips are split over the second half of A");
@@ -85,7 +96,8 @@ struct WsGeom {
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
-template <int RT, int R, int CG, int STAGES, bool FMA, int NWA = 8>
+// ACC: a later channel group, y_{k+1} += this group's terms (engine.cpp:157-162)
+template <int RT, int R, int CG, int STAGES, bool FMA, int NWA = 8, bool ACC = false>
 __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_constant__ FusedArgs a) {
     using G = WsGeom<RT, R, CG, STAGES, NWA>;
     using A = Arith<FMA>;
@@ -98,19 +110,21 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
     float* raw = smem;                      // [STAGES][NIN][FB]   TMA boxes
     float* produ = raw + G::RAW_FLOATS;     // [BH][BWU]           u
     float* prodp = produ + PBU;             // [CG][BH][BWP]       (F u, F^2 u)
-    float* xb = prodp + CG * PBP;           // [2][XBUF]           x-pass output
-    float* otile = xb + G::XB_FLOATS;       // [2][TY][TX]         output tiles (TMA store)
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(otile + G::OT_FLOATS);
+    float* xb = produ + G::PROD_FLOATS;     // [2][XBUF]           x-pass output
+    float* bslab = xb + G::XB_FLOATS;       // [NB/32][2][1+CG][8][TX] recombination slabs
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(bslab + G::IN_FLOATS);
     uint64_t* raw_full = mbar;             // [STAGES]  TMA -> A
     uint64_t* xb_full = mbar + STAGES;     // [2]       A -> B (count NA)
     uint64_t* xb_empty = mbar + STAGES + 2;  // [2]     B -> A (count NB)
+    uint64_t* slab_full = mbar + STAGES + 4;  // [NB/32][2] TMA -> B warp
 
     __shared__ IterState st;
     __shared__ PlaneStream prodq;
+    __shared__ PlaneStream slabq[NB / 32];
     __shared__ int prod_count;
 
     const int tid = threadIdx.x;
-    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    if (a.st->degenerate && SFK_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;
 
@@ -121,10 +135,14 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             mbar_init(&xb_full[b], NA);
             mbar_init(&xb_empty[b], NB);
         }
+        for (int w = 0; w < 2 * (NB / 32); ++w) mbar_init(&slab_full[w], 1);
         fence_barrier_init();
         prefetch_tensormap(&a.tm_x);
         prefetch_tensormap(&a.tm_sp);
         for (int c = 0; c < CG; ++c) prefetch_tensormap(&a.tm_f[c]);
+        prefetch_tensormap(&a.tm_out);
+        prefetch_tensormap(&a.tm_spc);
+        for (int c = 0; c < CG; ++c) prefetch_tensormap(&a.tm_fc[c]);
     }
     __syncthreads();
 
@@ -183,7 +201,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             // products over the halo box (engine.cpp:92-100): thread -> (row
             // lane pr0, float4 column pc4), rows pr0, pr0 + NPR, ... (constant
             // offsets, no index arithmetic in the loop)
-            if (pact) {
+            if (pact && !(SFK_EXP & 1)) {
                 const float4* rx = reinterpret_cast<const float4*>(rs) + pr0 * BW4 + pc4;
                 float* du = produ + pr0 * BWU + 4 * pc4;
                 float* dp = prodp + pr0 * BWP + 8 * pc4;
@@ -249,7 +267,8 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
-            if (xh == 0) {
+            if (SFK_EXP & 1) {
+            } else if (xh == 0) {
                 // u strips: rows xr0, xr0 + RL, ... of strip xs
                 const float* srcb = produ + xr0 * BWU + xs * G::SPU;
                 float* dstb = xbu + xr0 * TXU + xs * G::SPU;
@@ -322,9 +341,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         const int cp = bt & 15;    // columns 2cp, 2cp+1
         const int lane = bt & 31;
         const float inv_alpha = a.inv_alpha;
-        const bool first = a.first_group, last = a.last_group;
-        const long long plane_stride = static_cast<long long>(a.H) * a.pitch;
-        const int pitch = a.pitch;
+        const bool last = a.last_group;
 
         float2 ringu[4][K];          // (col 2cp, col 2cp+1) of u
         float2 ringp[CG][4][2][K];   // (F u, F^2 u) per column
@@ -343,55 +360,45 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
         int cnt = 0;   // in-volume planes consumed
-        int ecnt = 0;  // output planes emitted (selects the output tile)
-        // per-segment geometry (recomputed when the schedule moves to a new
-        // tile): element offsets of this thread's 4 rows inside a plane (rows
-        // past H are clamped so every load stays inside the buffer; their
-        // results are clipped by the TMA store and masked out of the sums)
-        int seg = -1, gband = 0, half = 0;
-        int roff[4];
-        bool rok[4], c1ok = false;
+        int ecnt = 0;  // output planes emitted
+        // This warp's 8 output rows: S^p / F_c (/ y so far) slabs come in by
+        // TMA a plane ahead into alternating buffers (cursor eq walks the
+        // emitted planes in schedule order); y_{k+1} overwrites the consumed
+        // S^p slab and leaves by TMA store. No CTA-wide barrier in B, and no
+        // edge masks: the TMA zero-fills S^p outside the volume, so those
+        // points come out as exactly 0 and add nothing to the sums, and the
+        // store clips them.
+        const int wb = bt >> 5;
+        float* myslab = bslab + wb * 2 * G::NSF * G::SLAB;
+        PlaneStream& eq = slabq[wb];  // lane 0 only (kept in shared memory: B is register-bound)
+        int eissued = 0;              // lane 0: slabs issued so far
+        auto issue_slab = [&]() {
+            if (eq.done) return;
+            const int sb = eissued & 1;
+            float* dst = myslab + sb * G::NSF * G::SLAB;
+            uint64_t* bar = &slab_full[2 * wb + sb];
+            const int x = eq.tile_x * TX, y = eq.tile_y * TY + 8 * wb, t = a.out_t0 + eq.p - a.buf_t0;
+            mbar_arrive_expect_tx(bar, G::NSF * G::SLAB * sizeof(float));
+            tma_load_3d(dst, &a.tm_spc, bar, x, y, t);
+#pragma unroll
+            for (int c = 0; c < CG; ++c) tma_load_3d(dst + (1 + c) * G::SLAB, &a.tm_fc[c], bar, x, y, t);
+            eq.next();
+            ++eissued;
+        };
+        if (lane == 0 && !(SFK_EXP & 4)) {
+            eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+            issue_slab();
+        }
+        const int sloff = ((band & 1) * 4) * TX + 2 * cp;  // this thread's rows in a slab
 
         // one plane with ring slot S_; the caller unrolls K planes so every
         // ring index is a compile-time constant (no rotation moves)
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
-            if (q.i != seg) {
-                seg = q.i;
-                const int y0 = q.tile_y * TY + band * 4;
-                const int x0 = q.tile_x * TX + 2 * cp;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    rok[r] = y0 + r < a.H && x0 < a.W;
-                    roff[r] = min(y0 + r, a.H - 1) * pitch + x0;
-                }
-                c1ok = x0 + 1 < a.W;
-                gband = q.tile_y * G::NBANDS + band;
-                half = q.tile_x;
-            }
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
-            const int out_p = q.p - RT;
-            const bool emit = out_p >= q.ta;
-            const int to = a.out_t0 + out_p;
-
-            // S^p and F_c of the output plane: pulled from L2 into L1 before the
-            // y-pass (TMA brought them in RT planes ago), read after it; holding
-            // them in registers across the y-pass would spill the ring
-            const float* spp = nullptr;
-            const float* fpp[CG];
-            if (emit) {
-                const long long po = static_cast<long long>(to - a.buf_t0) * plane_stride;
-                spp = a.sp + po;
-#pragma unroll
-                for (int c = 0; c < CG; ++c) fpp[c] = a.f[c] + po;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    prefetch_l1(spp + roff[r]);
-#pragma unroll
-                    for (int c = 0; c < CG; ++c) prefetch_l1(fpp[c] + roff[r]);
-                }
-            }
+            const bool emit = q.p - RT >= q.ta;
+            const int to = tg - RT;
 
             // y-pass (conv3d.cpp:113-135): first = w * in, then += (d ascending),
             // accumulated straight into this plane's ring slot
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 const float* xbp = xbu + XBU;
                 const float2* su = reinterpret_cast<const float2*>(xbu + (band * 4) * TXU) + cp;
 #pragma unroll
-                for (int j = 0; j < 4 + 2 * R; ++j) {
+                for (int j = 0; j < ((SFK_EXP & 2) ? 0 : 4 + 2 * R); ++j) {
                     const float2 vin = su[j * (TXU / 2)];
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < CG; ++c) {
+                for (int c = 0; c < ((SFK_EXP & 2) ? 0 : CG); ++c) {
                     const float4* sq =
                         reinterpret_cast<const float4*>(xbp + c * XBP + (band * 4) * TXQ) + cp;
 #pragma unroll
@@ -447,34 +454,40 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                         ringp[c][r][0][S_] = ringp[c][r][1][S_] = make_float2(0.0f, 0.0f);
                 }
             }
-            if (emit) {
-                float2 spv[4], fv[CG][4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    spv[r] = __ldg(reinterpret_cast<const float2*>(spp + roff[r]));
-#pragma unroll
-                    for (int c = 0; c < CG; ++c) fv[c][r] = __ldg(reinterpret_cast<const float2*>(fpp[c] + roff[r]));
+            if (emit && !(SFK_EXP & 4)) {
+                if (lane == 0) {
+                    // slab buffer of plane ecnt+1 = the one stored from at ecnt-1:
+                    // once that store has read it, fetch the next operands
+                    bulk_wait_read0();
+                    issue_slab();
                 }
-                float2 prev[4];
-                if (!first) {  // channel groups after the first add to y_{k+1}
-                    const float* op = a.out + static_cast<long long>(to - a.out_buf_t0) * plane_stride;
+                const int sb = ecnt & 1;
+                float* sl = myslab + sb * G::NSF * G::SLAB + sloff;
+                mbar_wait(&slab_full[2 * wb + sb], (ecnt >> 1) & 1);
+                float2 v2[4];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) prev[r] = *reinterpret_cast<const float2*>(op + roff[r]);
-                }
-                float* ot = otile + (ecnt & 1) * (TY * TX) + (band * 4) * TX + 2 * cp;
-                double cs0 = 0.0, cs1 = 0.0;
-                float cmax = 0.0f;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
+                for (int r = 0; r < ((SFK_EXP & 18) ? 0 : 4); ++r) {
                     // t-pass (conv3d.cpp:147-165): planes oldest..newest take
                     // taps_t[0..2RT]; first = w * in, then +=
                     float2 zu = A::mul2(a.taps_t[0], ringu[r][(S_ + 1) % K], zero2);
 #pragma unroll
                     for (int d = 1; d < K; ++d)
                         zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % K], one2, zero2);
-                    float v[2] = {0.0f, 0.0f};
+                    const float2 spv = *reinterpret_cast<const float2*>(sl + r * TX);
+                    float2 prev = make_float2(0.0f, 0.0f);
+                    if constexpr (ACC) {  // y so far (earlier groups); 0 outside the volume
+                        const int y = q.tile_y * TY + band * 4 + r, x = q.tile_x * TX + 2 * cp;
+                        if (y < a.H && x < a.W) {
+                            const float* op = a.out + static_cast<long long>(to - a.out_buf_t0) * a.H * a.pitch +
+                                              static_cast<long long>(y) * a.pitch + x;
+                            prev.x = op[0];
+                            if (x + 1 < a.W) prev.y = op[1];
+                        }
+                    }
+                    float v[2];
 #pragma unroll
-                    for (int c = 0; c < CG; ++c)
+                    for (int c = 0; c < CG; ++c) {
+                        const float2 fv = *reinterpret_cast<const float2*>(sl + (1 + c) * G::SLAB + r * TX);
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
                             float2 z = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % K], zero2);
@@ -482,49 +495,66 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                             for (int d = 1; d < K; ++d)
                                 z = A::mac2(z, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % K], one2, zero2);
                             // engine.cpp:113-119, channel sum engine.cpp:157-162
-                            const float term = A::recombine(j ? spv[r].y : spv[r].x,
-                                                            j ? fv[c][r].y : fv[c][r].x, inv_alpha,
-                                                            j ? zu.y : zu.x, z.y, z.x);
-                            v[j] = c > 0 ? xadd(v[j], term)
-                                         : (first ? term : xadd(j ? prev[r].y : prev[r].x, term));
+                            const float term = A::recombine(j ? spv.y : spv.x, j ? fv.y : fv.x,
+                                                            inv_alpha, j ? zu.y : zu.x, z.y, z.x);
+                            v[j] = c > 0 ? xadd(v[j], term) : (ACC ? xadd(j ? prev.y : prev.x, term) : term);
                         }
-                    *reinterpret_cast<float2*>(ot + r * TX) = make_float2(v[0], v[1]);
-                    // only points inside the volume enter the reductions
-                    const float v0 = rok[r] ? v[0] : 0.0f;
-                    const float v1 = (rok[r] && c1ok) ? v[1] : 0.0f;
-                    cs0 += static_cast<double>(v0) * static_cast<double>(v0);
-                    cs1 += static_cast<double>(v1) * static_cast<double>(v1);
-                    cmax = fmaxf(cmax, fmaxf(v0, v1));
+                    }
+                    v2[r] = make_float2(v[0], v[1]);
+                    // each thread overwrites exactly the S^p values it read
+                    *reinterpret_cast<float2*>(sl + r * TX) = v2[r];
                 }
-                // hand the tile to the TMA unit: generic-proxy writes -> async
-                // proxy, then one thread stores it (clipped at the volume edge).
-                // The store of tile e-2 (same buffer) was drained by the
-                // wait_group.read before the barrier of plane e-1.
+                // hand the slab to the TMA unit (generic-proxy writes -> async
+                // proxy; clipped at the volume edge)
                 fence_proxy_async();
-                if (bt == 0) bulk_wait_read0();
-                named_bar_sync(2, NB);
-                if (bt == 0) {
-                    tma_store_3d(&a.tm_out, otile + (ecnt & 1) * (TY * TX), q.tile_x * TX, q.tile_y * TY,
-                                 to - a.out_buf_t0);
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&a.tm_out, myslab + sb * G::NSF * G::SLAB, q.tile_x * TX,
+                                 q.tile_y * TY + 8 * wb, to - a.out_buf_t0);
                     bulk_commit();
                 }
                 ++ecnt;
-                if (last) {
+                if (last && !(SFK_EXP & 18)) {
                     // canonical reduction (device_common.cuh), warp-local: a warp
                     // holds two whole bands (lanes 0-15 band 2w, 16-31 band 2w+1),
-                    // lane l of a half holds columns 2l and 2l+1. The 32-column
-                    // butterfly (16, 8, 4, 2, 1) becomes xor 8, 4, 2, 1 over the
-                    // half-warp plus the final even+odd add inside the lane.
+                    // lane l of a half holds columns 2l and 2l+1: column sums over
+                    // the 4 rows, butterfly xor 8, 4, 2, 1 over the half-warp, then
+                    // even + odd column inside the lane. EXACT sums in fp64; FAST
+                    // in fp32 within the 4 x 32 block (fp64 above it).
+                    double sum;
+                    if constexpr (FMA) {
+                        float2 cs = make_float2(0.0f, 0.0f);
 #pragma unroll
-                    for (int o = 8; o >= 1; o >>= 1) {
-                        cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
-                        cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
+                        for (int r = 0; r < 4; ++r) cs = ffma2(v2[r], v2[r], cs);
+#pragma unroll
+                        for (int o = 8; o >= 1; o >>= 1) {
+                            const float2 t = make_float2(__shfl_xor_sync(0xffffffffu, cs.x, o),
+                                                         __shfl_xor_sync(0xffffffffu, cs.y, o));
+                            cs = make_float2(cs.x + t.x, cs.y + t.y);
+                        }
+                        sum = static_cast<double>(cs.x + cs.y);
+                    } else {
+                        double cs0 = 0.0, cs1 = 0.0;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            cs0 += static_cast<double>(v2[r].x) * static_cast<double>(v2[r].x);
+                            cs1 += static_cast<double>(v2[r].y) * static_cast<double>(v2[r].y);
+                        }
+#pragma unroll
+                        for (int o = 8; o >= 1; o >>= 1) {
+                            cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
+                            cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
+                        }
+                        sum = cs0 + cs1;
                     }
-                    const double sum = cs0 + cs1;
+                    float cmax = 0.0f;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) cmax = fmaxf(cmax, fmaxf(v2[r].x, v2[r].y));
                     const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
-                    if ((lane & 15) == 0 && gband < a.nbands && half < a.nhalves)
-                        a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gband) * a.nhalves +
-                               half] = sum;
+                    const int gb = q.tile_y * G::NBANDS + band;
+                    if ((lane & 15) == 0 && gb < a.nbands && q.tile_x < a.nhalves)
+                        a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves +
+                               q.tile_x] = sum;
                     if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
                 }
             }
@@ -542,7 +572,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             if constexpr (K > 7) { if (q.done) break; plane(integral_constant<int, (K > 7 ? 7 : 0)>{}); }
             if constexpr (K > 8) { if (q.done) break; plane(integral_constant<int, (K > 8 ? 8 : 0)>{}); }
         }
-        if (bt == 0) bulk_wait0();  // the output tiles are read before the CTA exits
+        if (lane == 0) bulk_wait0();  // the output slabs are written before the CTA exits
     }
 }
 

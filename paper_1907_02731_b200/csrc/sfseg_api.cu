@@ -186,6 +186,7 @@ struct FusedVariant {
     size_t smem;
     int threads;
     void (*kernel)(FusedArgs);
+    void (*kernel_acc)(FusedArgs);  // later channel groups (y += terms); may equal kernel
     int box_w, box_h;
 };
 
@@ -202,6 +203,7 @@ FusedVariant variant() {
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
     v.kernel = sfk::fused_step<RT, R, 1, TY, TX, QY, ST, FMA>;
+    v.kernel_acc = v.kernel;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
@@ -209,7 +211,10 @@ FusedVariant variant() {
 
 template <int RT, int R, bool FMA, int NWA = 8>
 FusedVariant variant_ws() {
-    using G = sfk::WsGeom<RT, R, 1, 2, NWA>;
+#ifndef SFK_STAGES
+#define SFK_STAGES 2
+#endif
+    using G = sfk::WsGeom<RT, R, 1, SFK_STAGES, NWA>;
     FusedVariant v;
     v.rt = RT;
     v.r = R;
@@ -218,7 +223,8 @@ FusedVariant variant_ws() {
     v.fma = FMA;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.kernel = sfk::fused_step_ws<RT, R, 1, 2, FMA, NWA>;
+    v.kernel = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, FMA, NWA, false>;
+    v.kernel_acc = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, FMA, NWA, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
@@ -566,7 +572,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         std::memset(&a, 0, sizeof a);
         a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
         a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
-        a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, v->ty);
+        a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, 8);
+        a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->tx, 8);
         a.sp = c->sp;
         a.out = out;
         a.part = c->part;
@@ -597,13 +604,15 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         static bool attr_set[64] = {};
         const int vidx = static_cast<int>(v - variants().data());
         if (!attr_set[vidx]) {
-            ck(cudaFuncSetAttribute(v->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(v->smem)),
-               "cudaFuncSetAttribute");
+            for (auto kfn : {v->kernel, v->kernel_acc})
+                ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(v->smem)),
+                   "cudaFuncSetAttribute");
             attr_set[vidx] = true;
         }
         for (size_t g = 0; g < Fch.size(); ++g) {
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+            a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->tx, 8);
             a.f[0] = Fch[g];
             a.first_group = g == 0;
             a.last_group = g + 1 == Fch.size();
@@ -613,7 +622,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                 cudaEventCreate(&e1);
                 cudaEventRecord(e0, c->stream);
             }
-            v->kernel<<<grid_n, v->threads, v->smem, c->stream>>>(a);
+            (g == 0 ? v->kernel : v->kernel_acc)<<<grid_n, v->threads, v->smem, c->stream>>>(a);
             launched(c->stream, "fused_step launch");
             if (c->timing) {
                 cudaEventRecord(e1, c->stream);

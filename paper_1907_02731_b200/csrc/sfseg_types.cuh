@@ -29,7 +29,9 @@ struct FusedArgs {
     CUtensorMap tm_x;           // iterate source y_k (or S / x0 at iteration 1)
     CUtensorMap tm_sp;          // S^p
     CUtensorMap tm_f[kMaxCG];   // feature channels of this group
-    CUtensorMap tm_out;         // y_{k+1}, box = one output tile (TMA store)
+    CUtensorMap tm_out;         // y_{k+1}, box = one warp's 8-row output slab (TMA store)
+    CUtensorMap tm_spc;         // S^p, box = one 8-row slab (recombination operands)
+    CUtensorMap tm_fc[kMaxCG];  // F_c, box = one 8-row slab
     const float* sp;            // pitched S^p (recombination reload)
     const float* f[kMaxCG];
     float* out;                 // pitched y_{k+1}
