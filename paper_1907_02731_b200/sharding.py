@@ -20,6 +20,10 @@ applied here with an all-reduce before the channels are loaded.
 A backend supplies steps 1, 4 and the device buffers; CudaBackend is the
 product (libsfseg_cuda.so). tests/ drive the same driver with a CPU oracle
 backend over gloo.
+
+Batches of independent clips (BASELINE configs[3]) need no exchange at all:
+assign_clips() packs them onto ranks by voxel count (longest processing time
+first) and every rank runs its own clips with its own context.
 """
 from __future__ import annotations
 
@@ -37,6 +41,39 @@ def shard_range(T: int, world: int, rank: int) -> Tuple[int, int]:
     base, rem = divmod(T, world)
     t0 = rank * base + min(rank, rem)
     return t0, t0 + base + (1 if rank < rem else 0)
+
+
+def assign_clips(voxels: Sequence[int], world: int) -> List[List[int]]:
+    """LPT bin-packing of independent clips onto `world` ranks by voxel count:
+    clips in decreasing size (ties by index) each go to the least-loaded rank
+    (ties by rank). Deterministic; returns the clip indices of every rank in
+    the order they were assigned."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    order = sorted(range(len(voxels)), key=lambda i: (-int(voxels[i]), i))
+    load = [0] * world
+    out: List[List[int]] = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda k: (load[k], k))
+        out[r].append(i)
+        load[r] += int(voxels[i])
+    return out
+
+
+def run_clips(problems, rank: int, world: int, ctx=None, arith: Optional[str] = None):
+    """Runs this rank's share of a batch of independent problems (clip
+    sharding, no collective). Returns {clip index: RunResult}."""
+    from . import engine as E
+
+    mine = assign_clips([p.voxels() for p in problems], world)[rank]
+    ctx = ctx or E.default_context()
+    out = {}
+    for i in mine:
+        prob = problems[i]
+        fs, _ = prob.generate()
+        cfg = prob.cfg if arith is None else E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith})
+        out[i] = E.run(fs, cfg, ctx=ctx)
+    return out
 
 
 def buffer_range(T: int, t0: int, t1: int, halo: int) -> Tuple[int, int]:

@@ -192,3 +192,75 @@ def test_run_is_normalize_of_step():
     stepped = E.sfseg_step(fs.unary, fs, cfg)
     want, _ = E.normalize_l2(stepped)
     assert _equal_values(res.soft, want)
+
+
+# --- the remaining BASELINE configs (c2, c3, c4), cropped so the reference
+# CPU run finishes in seconds; same channels, kernel and iteration count ---
+
+def _crop(fs, T, H, W):
+    sl = (slice(0, T), slice(0, H), slice(0, W))
+    return E.FeatureSet(np.ascontiguousarray(fs.unary[sl]),
+                        [np.ascontiguousarray(f[sl]) for f in fs.pairwise])
+
+
+def _ref_threads():
+    import os
+    return max(1, os.cpu_count() or 1)
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("idx,crop", [(2, (8, 96, 160)), (4, (10, 90, 150))])
+def test_run_multichannel_configs_cropped_match_reference(idx, crop, arith):
+    # c2: C=8, radii (3,7,7), box in t; c4: C=3, radii (4,10,10)
+    prob = synth.config(idx, frames=crop[0])[0]
+    fs, _ = prob.generate()
+    fs = _crop(fs, *crop)
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith})
+    cks = [1, 5, cfg.iterations]
+    snaps = {}
+    res = E.run(fs, cfg, observer=lambda it, x: snaps.__setitem__(it, x.copy()) if it in cks else None)
+    soft, mask, norms, ck = Reference().run(fs.unary, fs.pairwise, cfg, checkpoints=cks,
+                                            threads=_ref_threads())
+    for i, it in enumerate(cks):
+        _gate(snaps[it], ck[i], f"c{idx}{list(crop)} iter {it}")
+    _gate(res.soft, soft, f"c{idx} final")
+    _mask_gate(res.mask, mask, soft, cfg.final_threshold)
+    got = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
+    assert np.allclose(got, norms, rtol=1e-9 if arith == "exact" else 1e-5)
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+def test_run_c3_clips_match_reference():
+    # c3: independent clips (each its own problem, own norm); every clip of
+    # the batch T-cropped to 12 frames, full resolution
+    from paper_1907_02731_b200.sharding import run_clips
+
+    clips = synth.config(3, frames=12)[:4]
+    results = run_clips(clips, rank=0, world=1)  # the clip-sharded driver, one rank
+    assert sorted(results) == list(range(len(clips)))
+    for i, prob in enumerate(clips):
+        fs, _ = prob.generate()
+        res = results[i]
+        soft, mask, _, _ = Reference().run(fs.unary, fs.pairwise, prob.cfg, threads=_ref_threads())
+        _gate(res.soft, soft, prob.name)
+        _mask_gate(res.mask, mask, soft, prob.cfg.final_threshold)
+
+
+# radii beyond the fused instantiations run the generic multi-pass path; in
+# EXACT arithmetic it is bit-identical to the reference step as well
+GENERIC_CASES = [
+    ((5, 40, 70), 1.0, 0.1, (3, 7, 7), (1e30, 5.0, 5.0), 3),
+    ((9, 50, 60), 1.0, 0.1, (4, 10, 10), (0.5, 1.5, 1.5), 2),
+]
+
+
+@pytest.mark.parametrize("shape,alpha,p,radii,sigmas,C", GENERIC_CASES)
+def test_step_generic_path_bit_exact(shape, alpha, p, radii, sigmas, C):
+    S, F = _features(shape, 21, channels=C)
+    x = random_volume(shape, 98)
+    cfg = _cfg(radii, sigmas, alpha, p)
+    fs = E.FeatureSet(S, F)
+    got = E.sfseg_step(x, fs, cfg)
+    want = Oracle().step(x, S, F, cfg)
+    assert _equal_values(got, want)
