@@ -16,6 +16,12 @@ host buffers (H2D of S and F, solve, D2H of the soft iterate and mask inside
 the timed region). ``--impl reference`` times the reference's own CPU
 implementation (oracle/_ref/libsfseg_ref.so, compiled from the reference
 sources) on the host cores with a bounded sample of the same workload.
+
+Arithmetic: the headline (--arith fast, default) is fp32 with fused
+multiply-adds, inside the north star's parity gates (tests/test_gpu_parity.py);
+--arith exact reproduces the reference's separately rounded products and
+sums bit for bit (the step is bit-identical). On one GPU the line also carries
+the other mode's numbers under "other_arith".
 """
 from __future__ import annotations
 
@@ -189,10 +195,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--arith", default=os.environ.get("SFSEG_ARITH", "exact"),
+    ap.add_argument("--arith", default=os.environ.get("SFSEG_ARITH", "fast"),
                     choices=["exact", "fast"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-frames", type=int, default=4)
+    ap.add_argument("--ref-frames", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the time-sharded driver even on one GPU (testing)")
@@ -241,32 +247,43 @@ def main():
             dist.barrier()
 
     clocks = ClockSampler(local)
+    other = None  # the other arithmetic mode, measured the same way (1 GPU)
     if world == 1 and not args.sharded:
         ctx = E.Context(local)
         lib = ctx._lib
-        p = cfg.to_params()
-        fptrs = (C.c_void_p * Cn)(*[f.data_ptr() for f in F])
         # device-resident load (H2D once, outside the timed region)
+        fptrs = (C.c_void_p * Cn)(*[f.data_ptr() for f in F])
         N.check(lib.sfseg_load(ctx.handle, T, H, W, Cn, C.c_void_p(S.data_ptr()),
                                C.cast(fptrs, C.c_void_p), None, N.SFSEG_MEM_HOST))
-        for _ in range(args.warmup):
-            N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-        ctx.set_timing(True)
-        ctx.synchronize()
-        barrier()
-        solve_ms, kern_ms, launches = [], 0.0, 0
-        with clocks:
-            for _ in range(args.steps):
+
+        def timed_solves(arith, sampler=None):
+            c2 = E.SfsegConfig(**{**cfg.__dict__, "arith": arith})
+            p = c2.to_params()
+            for _ in range(args.warmup):
                 N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-                tm = ctx.timing()
-                solve_ms.append(tm.solve_ms)
-                kern_ms += tm.step_kernel_ms
-                launches += tm.step_launches
-        ctx.synchronize()
-        barrier()
-        ctx.set_timing(False)
-        total_ms = sum(solve_ms)
-        avg_launch_ms = kern_ms / max(1, launches)
+            ctx.set_timing(True)
+            ctx.synchronize()
+            barrier()
+            solve_ms, kern_ms, launches = [], 0.0, 0
+            import contextlib
+            with (sampler or contextlib.nullcontext()):
+                for _ in range(args.steps):
+                    N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
+                    tm = ctx.timing()
+                    solve_ms.append(tm.solve_ms)
+                    kern_ms += tm.step_kernel_ms
+                    launches += tm.step_launches
+            ctx.synchronize()
+            barrier()
+            ctx.set_timing(False)
+            return sum(solve_ms), kern_ms / max(1, launches)
+
+        total_ms, avg_launch_ms = timed_solves(args.arith, clocks)
+        oth = "exact" if args.arith == "fast" else "fast"
+        o_ms, o_launch = timed_solves(oth)
+        other = {"arith": oth, "value": nvox * iters * args.steps / (o_ms * 1e-3),
+                 "ms_per_step": o_ms / args.steps, "avg_launch_ms": o_launch}
+        p = cfg.to_params()
     else:
         # time-sharded: rank r owns frames [t0, t1) plus rt halo frames
         from paper_1907_02731_b200.sharding import (CudaBackend, ShardedSolver, buffer_range,
@@ -376,14 +393,18 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                         "kernel": "fused_step_exact", "avg_launch_ms": avg_launch_ms,
-                         "bytes_per_launch": bytes_per_launch},
+                         "kernel": f"fused_step_ws<RT={cfg.kernel.radii[0]},R={max(cfg.kernel.radii[1:])},"
+                                   f"{args.arith.upper()}>",
+                         "avg_launch_ms": avg_launch_ms, "bytes_per_launch": bytes_per_launch},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * iters * (Cn + 2),
         }
+        if other:
+            other["roofline_frac"] = bytes_per_launch / (other["avg_launch_ms"] * 1e-3) / 1e9 / peak
+            line["other_arith"] = other
         print(json.dumps(line), flush=True)
     if not sharded:
         ctx.close()
