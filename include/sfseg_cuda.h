@@ -4,11 +4,14 @@
  * This is the drop-in boundary for the reference's engine (proj/include/sfseg/
  * engine.hpp). Every entry point takes plain pointers and sizes; no C++, torch
  * or CUDA types cross it. The C++ shim in
- * paper_1907_02731_b200/csrc/engine_shim.cpp re-exports these calls as the
+ * paper_1907_02731_b200/csrc/shim/engine_shim.cpp re-exports these calls as the
  * seven symbols of the reference's engine.o (sfseg::SfsegConfig::validate,
  * sfseg_step_channel, sfseg_step, normalize_l2, project_binary,
- * threshold_final, run), so a reference build links the GPU engine instead of
- * engine.cpp without touching its headers or callers.
+ * threshold_final, run) and the five of conv3d.o (both make_gaussian_kernel
+ * overloads, convolve_separable, convolve_direct,
+ * separable_convolution_count), so a reference build links the GPU engine
+ * instead of engine.cpp / conv3d.cpp without touching its headers or callers
+ * (INTEGRATION.md).
  *
  * Volumes are dense float32, frame-major then row-major:
  *   index(t, y, x) = (t * H + y) * W + x        (volume.hpp:32-36)
@@ -51,9 +54,10 @@ enum sfseg_status {
  *         (conv3d.cpp:80-167, engine.cpp:92-119; the reference is built without
  *         FMA contraction). Outputs of a step are bit-identical to the CPU
  *         reference; the L2 norm differs only in the fp64 summation order.
- *  FAST:  fused multiply-adds and the cheaper y->x->t pass order; agrees with
- *         the reference within the north-star tolerance (max abs 1e-4,
- *         cosine >= 1-1e-6 after normalisation). */
+ *  FAST:  the same x -> y -> t passes with fused multiply-adds (and F*(F*u)
+ *         for the squared product); agrees with the reference within the
+ *         north-star tolerance (max abs 1e-4, cosine >= 1-1e-6 after
+ *         normalisation at every checkpoint). */
 enum sfseg_arith { SFSEG_ARITH_EXACT = 0, SFSEG_ARITH_FAST = 1 };
 
 enum sfseg_mem { SFSEG_MEM_HOST = 0, SFSEG_MEM_DEVICE = 1 };
