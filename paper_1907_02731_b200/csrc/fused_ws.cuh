@@ -39,17 +39,39 @@
 #define SFK_EXP 0
 #endif
 
+// timeline instrumentation (tools/trace_kernel.py; debug builds only):
+// clock64 at pipeline events of CTAs 0..3, planes 0..127
+#ifdef SFK_TRACE
+__device__ unsigned long long sfk_trace[4][128][16];
+#define SFK_T(pl, ev)                                                                   \
+    do {                                                                               \
+        if (blockIdx.x < 4 && (pl) < 128) sfk_trace[blockIdx.x][(pl)][(ev)] = clock64(); \
+    } while (0)
+#else
+#define SFK_T(pl, ev) \
+    do {              \
+    } while (0)
+#endif
+
 namespace sfk {
 
 template <int RT, int R, int CG, int STAGES, int NWA = 8>
 struct WsGeom {
     static constexpr int TY = 64, TX = 32;
     static constexpr int NA = 32 * NWA, NB = 256, NT = NA + NB;
-    // setmaxnreg budgets: the CTA pool is what the launch granted
-    // (65536 / NT rounded down to 8 per thread); asking for more deadlocks
-    static constexpr int RPOOL = (65536 / NT) / 8 * 8;
-    static constexpr int RA = NWA == 4 ? 80 : 56;
-    static constexpr int RB = ((NT * RPOOL - NA * RA) / NB) / 8 * 8;
+    // setmaxnreg budgets. Registers live in the 4 SMSP register files
+    // (512 per lane slot each); warp w runs on SMSP w % 4, and the launch
+    // grants every warp 512 / (most warps on one SMSP). Budgets must fit the
+    // fullest SMSP, or setmaxnreg.inc waits forever.
+    static constexpr int NWB = NB / 32;
+    static constexpr int WMAX = (NT / 32 + 3) / 4;
+    static constexpr int RPOOL = (512 / WMAX) / 8 * 8;
+#ifndef SFK_RA
+#define SFK_RA 56
+#endif
+    static constexpr int RA = NWA == 4 ? 80 : SFK_RA;
+    static constexpr int RB_SMSP = (512 - (NWA + 3) / 4 * RA) / ((NWB + 3) / 4);
+    static constexpr int RB = (RB_SMSP < 248 ? RB_SMSP : 248) / 8 * 8;
     static constexpr int K = 2 * RT + 1;
     static constexpr int NIN = 2 + CG;
     static constexpr int BH = TY + 2 * R;
@@ -89,6 +111,7 @@ struct WsGeom {
     static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
     static_assert(CG == 1 || true, "pair strips are split over the second half of A");
     static_assert(NA * RA + NB * RB <= NT * RPOOL, "register pool of the CTA");
+    static_assert((NWA + 3) / 4 * RA + (NWB + 3) / 4 * RB <= 512, "register file of one SMSP");
     static_assert(RB <= 248, "setmaxnreg range");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
     static_assert((BWU / 4) % 2 == 1 && (BWP / 4) % 2 == 1, "conflict-free product rows");
@@ -196,7 +219,9 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             const int tg = a.out_t0 + q.p;
             if (tg < 0 || tg >= a.T) continue;  // planes outside the volume: B zero-fills
             const int s = cnt % STAGES;
+            if (tid == 32) SFK_T(cnt, 0);
             mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
+            if (tid == 32) SFK_T(cnt, 1);
             const float* rs = raw + static_cast<size_t>(s) * NIN * FB;
             // products over the halo box (engine.cpp:92-100): thread -> (row
             // lane pr0, float4 column pc4), rows pr0, pr0 + NPR, ... (constant
@@ -258,6 +283,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 }
             }
             named_bar_sync(1, NA);  // products ready; raw stage s fully read
+            if (tid == 32) SFK_T(cnt, 2);
             if (tid == 0) {
                 fence_proxy_async();  // generic reads of stage s before the TMA overwrite
                 issue_next();
@@ -265,6 +291,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             // x-pass (conv3d.cpp:88-101) into the free x buffer
             const int b = cnt & 1;
             mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
+            if (tid == 32) SFK_T(cnt, 3);
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
             if (SFK_EXP & 1) {
@@ -327,8 +354,10 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     }
                 }
             }
+            if (tid == 32) SFK_T(cnt, 4);
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // every A thread is done with the products
+            if (tid == 32) SFK_T(cnt, 5);
             ++cnt;
         }
     } else {
@@ -404,7 +433,9 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             // accumulated straight into this plane's ring slot
             if (valid) {
                 const int b = cnt & 1;
+                if (bt == 0) SFK_T(cnt, 6);
                 mbar_wait(&xb_full[b], (cnt >> 1) & 1);
+                if (bt == 0) SFK_T(cnt, 7);
                 const float* xbu = xb + b * XBUF;
                 const float* xbp = xbu + XBU;
                 const float2* su = reinterpret_cast<const float2*>(xbu + (band * 4) * TXU) + cp;
@@ -443,6 +474,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                         }
                     }
                 }
+                if (bt == 0) SFK_T(cnt, 8);
                 mbar_arrive(&xb_empty[b]);
                 ++cnt;
             } else {
@@ -463,7 +495,9 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 }
                 const int sb = ecnt & 1;
                 float* sl = myslab + sb * G::NSF * G::SLAB + sloff;
+                if (bt == 0) SFK_T(ecnt, 9);
                 mbar_wait(&slab_full[2 * wb + sb], (ecnt >> 1) & 1);
+                if (bt == 0) SFK_T(ecnt, 10);
                 float2 v2[4];
 #pragma unroll
                 for (int r = 0; r < ((SFK_EXP & 18) ? 0 : 4); ++r) {
@@ -513,6 +547,8 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                                  q.tile_y * TY + 8 * wb, to - a.out_buf_t0);
                     bulk_commit();
                 }
+                if (bt == 0) SFK_T(ecnt, 11);
+                if (bt == 224) SFK_T(ecnt, 12);
                 ++ecnt;
                 if (last && !(SFK_EXP & 18)) {
                     // canonical reduction (device_common.cuh), warp-local: a warp

@@ -209,7 +209,10 @@ FusedVariant variant() {
     return v;
 }
 
-template <int RT, int R, bool FMA, int NWA = 8>
+#ifndef SFK_NWA
+#define SFK_NWA 8
+#endif
+template <int RT, int R, bool FMA, int NWA = SFK_NWA>
 FusedVariant variant_ws() {
 #ifndef SFK_STAGES
 #define SFK_STAGES 2
@@ -1440,3 +1443,9 @@ int sfseg_shard_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, 
 }
 
 }  // extern "C"
+
+#ifdef SFK_TRACE
+extern "C" int sfseg_debug_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, sfk_trace, sizeof(sfk_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
