@@ -175,7 +175,9 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else CUDA_LIB
+    # SFSEG_CUDA_LIB: another build of the same library (development aid for
+    # comparing kernel variants; still the CUDA library, never a fallback)
+    p = Path(path) if path else Path(os.environ.get("SFSEG_CUDA_LIB", CUDA_LIB))
     if not p.exists():
         raise CudaError(
             f"{p} is missing: run __graft_entry__.build() (nvcc, sm_100a); "

@@ -38,6 +38,11 @@
 #ifndef SFK_EXP
 #define SFK_EXP 0
 #endif
+// SFK_TMR=1: the t-pass ring of y-filtered planes lives in tensor memory
+// instead of B's registers
+#ifndef SFK_TMR
+#define SFK_TMR 0
+#endif
 
 // timeline instrumentation (tools/trace_kernel.py; debug builds only):
 // clock64 at pipeline events of CTAs 0..3, planes 0..127
@@ -71,7 +76,9 @@ struct WsGeom {
 #endif
     static constexpr int RA = NWA == 4 ? 80 : SFK_RA;
     static constexpr int RB_SMSP = (512 - (NWA + 3) / 4 * RA) / ((NWB + 3) / 4);
-    static constexpr int RB = (RB_SMSP < 248 ? RB_SMSP : 248) / 8 * 8;
+    static constexpr int RB_POOL = (NT * RPOOL - NA * RA) / NB;
+    static constexpr int RB_MIN = RB_SMSP < RB_POOL ? RB_SMSP : RB_POOL;
+    static constexpr int RB = (RB_MIN < 248 ? RB_MIN : 248) / 8 * 8;
     static constexpr int K = 2 * RT + 1;
     static constexpr int NIN = 2 + CG;
     static constexpr int BH = TY + 2 * R;
@@ -87,15 +94,21 @@ struct WsGeom {
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;
     static constexpr int XBP = (BH * TXQ + 31) / 32 * 32;
     static constexpr int XBUF = XBU + CG * XBP;  // one x-pass buffer
-    static constexpr int SPU = 4, SPP = 4;  // 8 u strips and 8 pair strips of 4 columns
-    static constexpr int NSU = TX / SPU, NSP = TX / SPP;
-    static constexpr int NINU = SPU + 2 * R, NINP = SPP + 2 * R;
+    // x-pass work split: the first NWU A warps take u strips of SU outputs
+    // (scalar FFMA), the others pair strips of SPP outputs (FFMA2, twice the
+    // FMA-pipe cycles per item: NWU : NWA - NWU = 3 : 5 balances them). A
+    // warp pass covers 8 consecutive rows x 4 strips; wide strips cut the
+    // shared-memory reads per output to (SU + 2R) / SU.
+    static constexpr int SU = 8, SPP = 8;
+    static constexpr int NSU = TX / SU, NSP = TX / SPP;
+    static constexpr int NINU = SU + 2 * R, NINP = SPP + 2 * R;
+    static constexpr int RBLK = (BH + 7) / 8;
+    static constexpr int UBLK = RBLK * (NSU / 4), PBLK = RBLK * (NSP / 4);
+    static constexpr int NWU = NWA == 8 ? 3 : NWA / 2;
+    static constexpr int UPASS = (UBLK + NWU - 1) / NWU, PPASSX = (PBLK + (NWA - NWU) - 1) / (NWA - NWU);
     static constexpr int NBANDS = TY / 4;
     // products: thread -> (row lane, float4 column); NPR rows per pass
     static constexpr int NPR = NA / BW4, PPASS = (BH + NPR - 1) / NPR;
-    // x-pass: half the A threads take the u strips, half the pair strips;
-    // in a half, thread -> (strip, row lane); RL rows per pass
-    static constexpr int NH = NA / 2, RL = NH / NSU, XPASS = (BH + RL - 1) / RL;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
     // (SFK_EXP bit 3, skeleton ablations only: no product / x-pass storage)
     static constexpr size_t PROD_FLOATS = (SFK_EXP & 8) ? 32 : size_t(PBU) + size_t(CG) * PBP;
@@ -107,7 +120,7 @@ struct WsGeom {
     static constexpr size_t IN_FLOATS = size_t(NB / 32) * 2 * NSF * SLAB;
     static constexpr size_t SMEM_BYTES =
         (RAW_FLOATS + PROD_FLOATS + XB_FLOATS + IN_FLOATS) * sizeof(float) + 256;
-    static_assert(NSU == NSP && NH % NSU == 0 && RL % 8 == 0, "x-pass thread mapping");
+    static_assert(NSU % 4 == 0 && NSP % 4 == 0, "x-pass passes: 4 strips x 8 rows");
     static_assert(NB == 16 * NBANDS, "B threads: 16 column pairs x 16 bands");
     static_assert(CG == 1 || true, "pair strips are split over the second half of A");
     static_assert(NA * RA + NB * RB <= NT * RPOOL, "register pool of the CTA");
@@ -144,6 +157,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
     __shared__ IterState st;
     __shared__ PlaneStream prodq;
     __shared__ PlaneStream slabq[NB / 32];
+    __shared__ uint32_t tmem_base_sh;
     __shared__ int prod_count;
 
     const int tid = threadIdx.x;
@@ -209,8 +223,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
 
         const int pr0 = tid / BW4, pc4 = tid - (tid / BW4) * BW4;
         const bool pact = tid < G::NPR * BW4;
-        const int xh = tid / G::NH, xt = tid - xh * G::NH;
-        const int xs = xt / G::RL, xr0 = xt - xs * G::RL;
+        const int xw = tid >> 5, xl = tid & 31;  // x-pass: warp, lane (row xl & 7, strip xl >> 3)
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
@@ -295,15 +308,17 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
             if (SFK_EXP & 1) {
-            } else if (xh == 0) {
-                // u strips: rows xr0, xr0 + RL, ... of strip xs
-                const float* srcb = produ + xr0 * BWU + xs * G::SPU;
-                float* dstb = xbu + xr0 * TXU + xs * G::SPU;
+            } else if (xw < G::NWU) {
+                // u strips: pass k covers row block / strip group blk
 #pragma unroll
-                for (int k = 0; k < G::XPASS; ++k) {
-                    if (k == G::XPASS - 1 && xr0 + k * G::RL >= BH) break;
-                    const float4* src = reinterpret_cast<const float4*>(srcb + k * G::RL * BWU);
-                    float o[G::SPU];
+                for (int k = 0; k < G::UPASS; ++k) {
+                    const int blk = xw + k * G::NWU;
+                    if (blk >= G::UBLK) break;
+                    const int r = (blk / (G::NSU / 4)) * 8 + (xl & 7);
+                    const int st = (blk % (G::NSU / 4)) * 4 + (xl >> 3);
+                    if (r >= BH) continue;
+                    const float4* src = reinterpret_cast<const float4*>(produ + r * BWU + st * G::SU);
+                    float o[G::SU];
                     float4 q4;
 #pragma unroll
                     for (int m4 = 0; m4 < (G::XOFF + G::NINU + 3) / 4 * 4; ++m4) {
@@ -313,23 +328,30 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                         const float vin = (m4 % 4 == 0) ? q4.x : (m4 % 4 == 1) ? q4.y
                                         : (m4 % 4 == 2) ? q4.z : q4.w;
 #pragma unroll
-                        for (int j = 0; j < G::SPU; ++j) {
+                        for (int j = 0; j < G::SU; ++j) {
                             const int d = m - j;
                             if (d < 0 || d > 2 * R) continue;
                             o[j] = d == 0 ? A::mul(a.taps_x[0], vin) : A::mac(o[j], a.taps_x[d], vin);
                         }
                     }
-                    *reinterpret_cast<float4*>(dstb + k * G::RL * TXU) = make_float4(o[0], o[1], o[2], o[3]);
+                    float4* dst = reinterpret_cast<float4*>(xbu + r * TXU + st * G::SU);
+#pragma unroll
+                    for (int v = 0; v < G::SU / 4; ++v)
+                        dst[v] = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
                 }
             } else {
+                const int wp = xw - G::NWU;
 #pragma unroll
-                for (int c = 0; c < CG; ++c) {
-                    const float* srcb = prodp + c * PBP + xr0 * BWP + 2 * xs * G::SPP;
-                    float* dstb = xbp + c * XBP + xr0 * TXQ + 2 * xs * G::SPP;
+                for (int k = 0; k < G::PPASSX; ++k) {
+                    const int blk = wp + k * (NA / 32 - G::NWU);
+                    if (blk >= G::PBLK) break;
+                    const int r = (blk / (G::NSP / 4)) * 8 + (xl & 7);
+                    const int st = (blk % (G::NSP / 4)) * 4 + (xl >> 3);
+                    if (r >= BH) continue;
 #pragma unroll
-                    for (int k = 0; k < G::XPASS; ++k) {
-                        if (k == G::XPASS - 1 && xr0 + k * G::RL >= BH) break;
-                        const float4* src = reinterpret_cast<const float4*>(srcb + k * G::RL * BWP);
+                    for (int c = 0; c < CG; ++c) {
+                        const float4* src =
+                            reinterpret_cast<const float4*>(prodp + c * PBP + r * BWP + 2 * st * G::SPP);
                         float2 o[G::SPP];
                         float4 q4;
 #pragma unroll
@@ -348,7 +370,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                             }
                         }
                         // float2 stores straight from the FFMA2 register pairs
-                        float2* dst = reinterpret_cast<float2*>(dstb + k * G::RL * TXQ);
+                        float2* dst = reinterpret_cast<float2*>(xbp + c * XBP + r * TXQ + 2 * st * G::SPP);
 #pragma unroll
                         for (int j = 0; j < G::SPP; ++j) dst[j] = o[j];
                     }
@@ -372,12 +394,14 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         const float inv_alpha = a.inv_alpha;
         const bool last = a.last_group;
 
-        float2 ringu[4][K];          // (col 2cp, col 2cp+1) of u
-        float2 ringp[CG][4][2][K];   // (F u, F^2 u) per column
+        constexpr bool TMR = SFK_TMR != 0;
+        constexpr int KR = TMR ? 1 : K;  // register ring depth
+        float2 ringu[4][KR];          // (col 2cp, col 2cp+1) of u
+        float2 ringp[CG][4][2][KR];   // (F u, F^2 u) per column
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
+            for (int k = 0; k < KR; ++k) {
                 ringu[r][k] = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int c = 0; c < CG; ++c) {
@@ -385,6 +409,20 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     ringp[c][r][1][k] = make_float2(0.0f, 0.0f);
                 }
             }
+        // TMEM ring (TMR): each B thread keeps K slots of RW = 8 + 16 CG words
+        // in its TMEM lane; warps w and w+4 share a lane quadrant and split the
+        // columns into two halves of 128
+        constexpr int RW = 8 + 16 * CG;
+        static_assert(!TMR || K * RW <= 128, "TMEM ring of one thread");
+        uint32_t tm_ring = 0;
+        if constexpr (TMR) {
+            if (bt < 32) tmem_alloc<256>(&tmem_base_sh);
+            tcgen05_fence_before();
+            named_bar_sync(3, NB);
+            tcgen05_fence_after();
+            const int wq = (NA / 32 + (bt >> 5)) & 3;  // CTA warp id % 4
+            tm_ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) + static_cast<uint32_t>(((bt >> 5) >> 2) * 128);
+        }
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
@@ -424,6 +462,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
         // ring index is a compile-time constant (no rotation moves)
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
+            constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const bool emit = q.p - RT >= q.ta;
@@ -446,8 +485,8 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     for (int r = 0; r < 4; ++r) {
                         const int d = j - r;
                         if (d < 0 || d > 2 * R) continue;
-                        ringu[r][S_] = d == 0 ? A::mul2(a.taps_y[0], vin, zero2)
-                                              : A::mac2(ringu[r][S_], a.taps_y[d], vin, one2, zero2);
+                        ringu[r][SR] = d == 0 ? A::mul2(a.taps_y[0], vin, zero2)
+                                              : A::mac2(ringu[r][SR], a.taps_y[d], vin, one2, zero2);
                     }
                 }
 #pragma unroll
@@ -463,13 +502,13 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                             const int d = j - r;
                             if (d < 0 || d > 2 * R) continue;
                             if (d == 0) {
-                                ringp[c][r][0][S_] = A::mul2(a.taps_y[0], v0, zero2);
-                                ringp[c][r][1][S_] = A::mul2(a.taps_y[0], v1, zero2);
+                                ringp[c][r][0][SR] = A::mul2(a.taps_y[0], v0, zero2);
+                                ringp[c][r][1][SR] = A::mul2(a.taps_y[0], v1, zero2);
                             } else {
-                                ringp[c][r][0][S_] =
-                                    A::mac2(ringp[c][r][0][S_], a.taps_y[d], v0, one2, zero2);
-                                ringp[c][r][1][S_] =
-                                    A::mac2(ringp[c][r][1][S_], a.taps_y[d], v1, one2, zero2);
+                                ringp[c][r][0][SR] =
+                                    A::mac2(ringp[c][r][0][SR], a.taps_y[d], v0, one2, zero2);
+                                ringp[c][r][1][SR] =
+                                    A::mac2(ringp[c][r][1][SR], a.taps_y[d], v1, one2, zero2);
                             }
                         }
                     }
@@ -480,11 +519,36 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             } else {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    ringu[r][S_] = make_float2(0.0f, 0.0f);
+                    ringu[r][SR] = make_float2(0.0f, 0.0f);
 #pragma unroll
                     for (int c = 0; c < CG; ++c)
-                        ringp[c][r][0][S_] = ringp[c][r][1][S_] = make_float2(0.0f, 0.0f);
+                        ringp[c][r][0][SR] = ringp[c][r][1][SR] = make_float2(0.0f, 0.0f);
                 }
+            }
+            if constexpr (TMR) {
+                // this plane's slot: u (8 words), then (F u, F^2 u) per channel
+                // (16 words); the slot it replaces held a plane no longer needed
+                float w8[8];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    w8[2 * r] = ringu[r][0].x;
+                    w8[2 * r + 1] = ringu[r][0].y;
+                }
+                tmem_st8(tm_ring + S_ * RW, w8);
+#pragma unroll
+                for (int c = 0; c < CG; ++c)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr) {
+                            const int r = 2 * h + rr;
+                            w8[4 * rr] = ringp[c][r][0][0].x;
+                            w8[4 * rr + 1] = ringp[c][r][0][0].y;
+                            w8[4 * rr + 2] = ringp[c][r][1][0].x;
+                            w8[4 * rr + 3] = ringp[c][r][1][0].y;
+                        }
+                        tmem_st8(tm_ring + S_ * RW + 8 + 16 * c + 8 * h, w8);
+                    }
             }
             if (emit && !(SFK_EXP & 4)) {
                 if (lane == 0) {
@@ -499,14 +563,72 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                 mbar_wait(&slab_full[2 * wb + sb], (ecnt >> 1) & 1);
                 if (bt == 0) SFK_T(ecnt, 10);
                 float2 v2[4];
+                // TMR: t-pass (conv3d.cpp:147-165) over the TMEM slots, oldest
+                // first (taps_t[0..2RT], first = w * in, then +=); the newest
+                // plane is still in registers
+                float2 tu[4], tp[CG][4][2];
+                if constexpr (TMR) {
+                    tmem_wait_st();
+#pragma unroll
+                    for (int d = 0; d < K; ++d) {
+                        const int sl = (S_ + 1 + d) % K;
+                        float2 lu[4], lp[CG][4][2];
+                        if (sl == S_) {
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                lu[r] = ringu[r][0];
+#pragma unroll
+                                for (int c = 0; c < CG; ++c) {
+                                    lp[c][r][0] = ringp[c][r][0][0];
+                                    lp[c][r][1] = ringp[c][r][1][0];
+                                }
+                            }
+                        } else {
+                            float w8[1 + 2 * CG][8];
+                            tmem_ld8(tm_ring + sl * RW, w8[0]);
+#pragma unroll
+                            for (int c = 0; c < CG; ++c) {
+                                tmem_ld8(tm_ring + sl * RW + 8 + 16 * c, w8[1 + 2 * c]);
+                                tmem_ld8(tm_ring + sl * RW + 16 + 16 * c, w8[2 + 2 * c]);
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                lu[r] = make_float2(w8[0][2 * r], w8[0][2 * r + 1]);
+#pragma unroll
+                                for (int c = 0; c < CG; ++c) {
+                                    const float* q8 = w8[1 + 2 * c + (r >> 1)] + 4 * (r & 1);
+                                    lp[c][r][0] = make_float2(q8[0], q8[1]);
+                                    lp[c][r][1] = make_float2(q8[2], q8[3]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            tu[r] = d == 0 ? A::mul2(a.taps_t[0], lu[r], zero2)
+                                           : A::mac2(tu[r], a.taps_t[d], lu[r], one2, zero2);
+#pragma unroll
+                            for (int c = 0; c < CG; ++c)
+#pragma unroll
+                                for (int j = 0; j < 2; ++j)
+                                    tp[c][r][j] = d == 0 ? A::mul2(a.taps_t[0], lp[c][r][j], zero2)
+                                                         : A::mac2(tp[c][r][j], a.taps_t[d], lp[c][r][j], one2, zero2);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < ((SFK_EXP & 18) ? 0 : 4); ++r) {
                     // t-pass (conv3d.cpp:147-165): planes oldest..newest take
                     // taps_t[0..2RT]; first = w * in, then +=
-                    float2 zu = A::mul2(a.taps_t[0], ringu[r][(S_ + 1) % K], zero2);
+                    float2 zu;
+                    if constexpr (TMR) {
+                        zu = tu[r];
+                    } else {
+                        zu = A::mul2(a.taps_t[0], ringu[r][(S_ + 1) % KR], zero2);
 #pragma unroll
-                    for (int d = 1; d < K; ++d)
-                        zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % K], one2, zero2);
+                        for (int d = 1; d < K; ++d)
+                            zu = A::mac2(zu, a.taps_t[d], ringu[r][(S_ + 1 + d) % KR], one2, zero2);
+                    }
                     const float2 spv = *reinterpret_cast<const float2*>(sl + r * TX);
                     float2 prev = make_float2(0.0f, 0.0f);
                     if constexpr (ACC) {  // y so far (earlier groups); 0 outside the volume
@@ -524,10 +646,15 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                         const float2 fv = *reinterpret_cast<const float2*>(sl + (1 + c) * G::SLAB + r * TX);
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
-                            float2 z = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % K], zero2);
+                            float2 z;
+                            if constexpr (TMR) {
+                                z = tp[c][r][j];
+                            } else {
+                                z = A::mul2(a.taps_t[0], ringp[c][r][j][(S_ + 1) % KR], zero2);
 #pragma unroll
-                            for (int d = 1; d < K; ++d)
-                                z = A::mac2(z, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % K], one2, zero2);
+                                for (int d = 1; d < K; ++d)
+                                    z = A::mac2(z, a.taps_t[d], ringp[c][r][j][(S_ + 1 + d) % KR], one2, zero2);
+                            }
                             // engine.cpp:113-119, channel sum engine.cpp:157-162
                             const float term = A::recombine(j ? spv.y : spv.x, j ? fv.y : fv.x,
                                                             inv_alpha, j ? zu.y : zu.x, z.y, z.x);
@@ -609,6 +736,13 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
             if constexpr (K > 8) { if (q.done) break; plane(integral_constant<int, (K > 8 ? 8 : 0)>{}); }
         }
         if (lane == 0) bulk_wait0();  // the output slabs are written before the CTA exits
+        if constexpr (TMR) {
+            tmem_wait_st();
+            tcgen05_fence_before();
+            named_bar_sync(3, NB);
+            tcgen05_fence_after();
+            if (bt < 32) tmem_dealloc<256>(tmem_base_sh);
+        }
     }
 }
 
