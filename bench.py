@@ -300,6 +300,7 @@ def main():
         for _ in range(args.warmup):
             solver.solve_only(cfg)
         barrier()
+        be.ctx.set_timing(True)  # per-launch events of this rank's fused kernel
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with clocks:
             ev0.record()
@@ -310,8 +311,11 @@ def main():
             ev1.record()
             torch.cuda.synchronize()
         total_ms = ev0.elapsed_time(ev1)
+        kms, kn = C.c_double(), C.c_int32()
+        N.check(be.lib.sfseg_ctx_kernel_time(be.ctx.handle, C.byref(kms), C.byref(kn)))
+        be.ctx.set_timing(False)
         barrier()
-        avg_launch_ms = float("nan")
+        avg_launch_ms = kms.value / max(1, kn.value)
     if dist:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -321,9 +325,12 @@ def main():
     # roofline of the dominant kernel (fused stencil): algorithmic bytes per
     # launch = 4 B x (x, S^p, F_c reads + one write) per voxel, one launch per
     # channel group
-    bytes_per_launch = 4.0 * (Cn + 3) * nvox if Cn == 1 else 4.0 * 4 * nvox
     sharded = world > 1 or args.sharded
-    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9 if not sharded else float("nan")
+    # (time-sharded: rank 0's launch over its own output frames; recomputed
+    # halo frames are not algorithmic bytes)
+    unit_vox = nvox if not sharded else (t1 - t0) * H * W
+    bytes_per_launch = 4.0 * (Cn + 3) * unit_vox if Cn == 1 else 4.0 * 4 * unit_vox
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     peak, peak_kind = _peaks()
     traffic = None
     tfile = ROOT / "profiles" / f"traffic_c{args.config}_{args.arith}.json"
@@ -347,11 +354,15 @@ def main():
         h2d = (1 + Cn) * nvox * 4
         d2h = nvox * 4 + nvox
     else:
+        soft = torch.empty((t1 - t0, H, W), dtype=torch.float32, pin_memory=True)
+        mask = torch.empty((t1 - t0, H, W), dtype=torch.uint8, pin_memory=True)
         for i in range(args.e2e_steps + 1):
             barrier()
             t_0 = time.perf_counter()
-            solver.load(T, H, W, S[b0:b1], [f[b0:b1] for f in F], None, halo)
-            solver.run(cfg)
+            dS = S[b0:b1].to("cuda", non_blocking=True)
+            dF = [f[b0:b1].to("cuda", non_blocking=True) for f in F]
+            solver.load(T, H, W, dS, dF, None, halo)
+            solver.run(cfg, out=(soft.numpy(), mask.numpy()))
             if i > 0:
                 e2e_t.append(time.perf_counter() - t_0)
         h2d = (1 + Cn) * (b1 - b0) * H * W * 4 * world

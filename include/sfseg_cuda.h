@@ -131,6 +131,10 @@ int sfseg_ctx_set_timing(sfseg_ctx* ctx, int enabled);
 int sfseg_ctx_get_timing(const sfseg_ctx* ctx, sfseg_timing* out);
 /* Blocks until the context stream is idle. */
 int sfseg_ctx_synchronize(sfseg_ctx* ctx);
+/* Sum of the fused-step kernel times (CUDA events on the context stream)
+ * recorded since timing was enabled or since the last call, and their count;
+ * consumes the records. Used to time time-sharded solves (sfseg_shard_step). */
+int sfseg_ctx_kernel_time(sfseg_ctx* ctx, double* ms, int32_t* launches);
 /* The context's cudaStream_t (as void*), for ordering NCCL work against it. */
 void* sfseg_ctx_stream(sfseg_ctx* ctx);
 

@@ -139,6 +139,7 @@ _SIGS = {
     "sfseg_ctx_set_timing": (C.c_int, [_P, C.c_int]),
     "sfseg_ctx_get_timing": (C.c_int, [_P, C.POINTER(Timing)]),
     "sfseg_ctx_synchronize": (C.c_int, [_P]),
+    "sfseg_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "sfseg_ctx_stream": (C.c_void_p, [_P]),
     "sfseg_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, _I32]),
     "sfseg_solve": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, C.POINTER(IterRecord)]),

@@ -248,6 +248,17 @@ __global__ void k_max(Vol v, float* out) {
 }
 
 // mask_from_volume with cut = float(frac * max) (engine.cpp:212, volume.cpp:107-114)
+// dense <-> pitched copy of `rows` rows of w floats (host transfers stage
+// through a dense buffer so the DMA runs as one contiguous copy)
+__global__ void k_repitch(const float* __restrict__ src, int src_pitch, float* __restrict__ dst,
+                          int dst_pitch, size_t rows, int w) {
+    for (size_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* s = src + r * src_pitch;
+        float* d = dst + r * dst_pitch;
+        for (int x = threadIdx.x; x < w; x += blockDim.x) d[x] = s[x];
+    }
+}
+
 __global__ void k_mask(Vol v, const float* maxp, double frac, uint8_t* mask) {
     const float cut = static_cast<float>(frac * static_cast<double>(*maxp));
     SFK_FOR_VOXELS(v, t, y, x) {

@@ -352,6 +352,12 @@ struct sfseg_ctx {
     long long sched_key = -1;
     // generic-path temporaries (allocated lazily)
     std::vector<float*> tmp;
+    // dense staging for host transfers (one contiguous DMA, re-pitched on the
+    // device) and the device mask of downloads
+    float* stage = nullptr;
+    size_t stage_elems = 0;
+    uint8_t* dmask = nullptr;
+    size_t dmask_elems = 0;
     // timing
     bool timing = false;
     sfseg_timing last_timing{};
@@ -398,6 +404,12 @@ void release_problem(sfseg_ctx* c) {
     dfree(c->y[1]);
     for (auto*& t : c->tmp) dfree(t);
     c->tmp.clear();
+    if (c->stage) cudaFree(c->stage);
+    if (c->dmask) cudaFree(c->dmask);
+    c->stage = nullptr;
+    c->stage_elems = 0;
+    c->dmask = nullptr;
+    c->dmask_elems = 0;
     if (c->part) cudaFree(c->part);
     if (c->frame_sum) cudaFree(c->frame_sum);
     if (c->frame_max) cudaFree(c->frame_max);
@@ -451,21 +463,50 @@ void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int 
 }
 
 // dense (T,H,W) host/device -> pitched device
+float* stage_buf(sfseg_ctx* c) {
+    const size_t n = static_cast<size_t>(c->T) * c->H * c->W;
+    if (c->stage_elems < n) {
+        if (c->stage) cudaFree(c->stage);
+        c->stage = nullptr;
+        c->stage_elems = 0;
+        ck(cudaMalloc(&c->stage, n * sizeof(float)), "cudaMalloc staging");
+        c->stage_elems = n;
+    }
+    return c->stage;
+}
+
+// Host volumes move as one dense DMA through a staging buffer and are
+// (re)pitched on the device at HBM speed; a 2-D copy of W-float rows would
+// run the DMA engine one short row at a time.
 void upload(sfseg_ctx* c, float* dst, const float* src, int32_t mem) {
-    const cudaMemcpyKind kind = mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice
-                                                        : cudaMemcpyHostToDevice;
-    ck(cudaMemcpy2DAsync(dst, c->P * sizeof(float), src, c->W * sizeof(float),
-                         c->W * sizeof(float), static_cast<size_t>(c->T) * c->H, kind,
-                         c->stream),
+    const size_t rows = static_cast<size_t>(c->T) * c->H;
+    if (mem == SFSEG_MEM_DEVICE || c->P == c->W) {
+        ck(cudaMemcpy2DAsync(dst, c->P * sizeof(float), src, c->W * sizeof(float), c->W * sizeof(float),
+                             rows, mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             c->stream),
+           "upload volume");
+        return;
+    }
+    float* st = stage_buf(c);
+    ck(cudaMemcpyAsync(st, src, rows * c->W * sizeof(float), cudaMemcpyHostToDevice, c->stream),
        "upload volume");
+    sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(st, c->W, dst, c->P, rows, c->W);
+    launched(c->stream, "k_repitch");
 }
 
 void download(sfseg_ctx* c, float* dst, const float* src, int32_t mem) {
-    const cudaMemcpyKind kind = mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice
-                                                        : cudaMemcpyDeviceToHost;
-    ck(cudaMemcpy2DAsync(dst, c->W * sizeof(float), src, c->P * sizeof(float),
-                         c->W * sizeof(float), static_cast<size_t>(c->T) * c->H, kind,
-                         c->stream),
+    const size_t rows = static_cast<size_t>(c->T) * c->H;
+    if (mem == SFSEG_MEM_DEVICE || c->P == c->W) {
+        ck(cudaMemcpy2DAsync(dst, c->W * sizeof(float), src, c->P * sizeof(float), c->W * sizeof(float),
+                             rows, mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             c->stream),
+           "download volume");
+        return;
+    }
+    float* st = stage_buf(c);
+    sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(src, c->P, st, c->W, rows, c->W);
+    launched(c->stream, "k_repitch");
+    ck(cudaMemcpyAsync(dst, st, rows * c->W * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
        "download volume");
 }
 
@@ -845,13 +886,20 @@ void mask_of(sfseg_ctx* c, float* v, double frac, uint8_t* mask, int32_t mem) {
     float* mx = max_of(c, v);
     const size_t n = static_cast<size_t>(c->T) * c->H * c->W;
     uint8_t* dm = reinterpret_cast<uint8_t*>(mem == SFSEG_MEM_DEVICE ? mask : nullptr);
-    if (!dm) ck(cudaMallocAsync(reinterpret_cast<void**>(&dm), n, c->stream), "malloc mask");
+    if (!dm) {  // persistent device mask for host downloads
+        if (c->dmask_elems < n) {
+            if (c->dmask) cudaFree(c->dmask);
+            c->dmask = nullptr;
+            c->dmask_elems = 0;
+            ck(cudaMalloc(reinterpret_cast<void**>(&c->dmask), n), "malloc mask");
+            c->dmask_elems = n;
+        }
+        dm = c->dmask;
+    }
     sfk::k_mask<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(v), mx, frac, dm);
     launched(c->stream, "k_mask");
-    if (mem != SFSEG_MEM_DEVICE) {
+    if (mem != SFSEG_MEM_DEVICE)
         ck(cudaMemcpyAsync(mask, dm, n, cudaMemcpyDeviceToHost, c->stream), "mask D2H");
-        ck(cudaFreeAsync(dm, c->stream), "free");
-    }
 }
 
 }  // namespace
@@ -951,6 +999,26 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         for (auto e : c->ev) cudaEventDestroy(e);
         cudaStreamDestroy(c->stream);
         delete c;
+    });
+}
+
+int sfseg_ctx_kernel_time(sfseg_ctx* c, double* ms, int32_t* launches) {
+    return guarded([&] {
+        if (!c || !ms || !launches) fail(SFSEG_ERR_PARAMETER, "null argument");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        double total = 0.0;
+        int n = 0;
+        for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
+            float m = 0.0f;
+            cudaEventElapsedTime(&m, c->ev[i], c->ev[i + 1]);
+            total += m;
+            ++n;
+        }
+        for (auto e : c->ev) cudaEventDestroy(e);
+        c->ev.clear();
+        *ms = total;
+        *launches = n;
     });
 }
 

@@ -170,9 +170,12 @@ class CudaBackend:
         self._keep_gathered.clear()
         return list(out)
 
-    def download(self, frac, t0, t1):
-        soft = np.empty((t1 - t0, self.H, self.W), np.float32)
-        mask = np.empty((t1 - t0, self.H, self.W), np.uint8)
+    def download(self, frac, t0, t1, out=None):
+        if out is not None:  # caller-provided (e.g. pinned) host arrays
+            soft, mask = out
+        else:
+            soft = np.empty((t1 - t0, self.H, self.W), np.float32)
+            mask = np.empty((t1 - t0, self.H, self.W), np.uint8)
         N.check(self.lib.sfseg_shard_download(self.ctx.handle, float(frac),
                                               C.c_void_p(soft.ctypes.data),
                                               C.c_void_p(mask.ctypes.data), N.SFSEG_MEM_HOST))
@@ -252,7 +255,9 @@ class ShardedSolver:
             parts.append(bufs[r][: b - a])
         return torch.cat(parts).contiguous()  # frame order
 
-    def run(self, cfg) -> Tuple[np.ndarray, np.ndarray, List[float]]:
+    def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
+        """out: optional preallocated host (soft, mask) arrays for this rank's
+        frames (the download lands there)."""
         import torch
 
         params = cfg.to_params()
@@ -266,7 +271,10 @@ class ShardedSolver:
             self.b.after_exchange()
             self.b.finalize(params, it, fs, fm)
         norms = self.b.norms(cfg.iterations)
-        soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1)
+        if out is not None:
+            soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1, out=out)
+        else:
+            soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1)
         return soft, mask, norms
 
     def solve_only(self, cfg) -> None:
