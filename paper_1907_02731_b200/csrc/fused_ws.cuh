@@ -252,6 +252,12 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     const int i = k * G::NPR * BW4;
                     const float4 yv = rx[i];
                     const float4 sv = rx[FB / 4 + i];
+                    // EXACT: the F load goes out with the others (2% faster);
+                    // FAST: issuing all of them up front floods the shared-
+                    // memory queue the B warps' y-pass shares (measured 40%
+                    // slower), so F is loaded where it is used
+                    float4 fpre = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if constexpr (!FMA) fpre = rx[2 * (FB / 4) + i];
                     float4 xv;
                     if (sigm) {
                         xv.x = A::load_sigmoid(yv.x, st);
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
                     *reinterpret_cast<float4*>(du + k * G::NPR * BWU) = u;
 #pragma unroll
                     for (int cg = 0; cg < CG; ++cg) {
-                        const float4 fv = rx[(2 + cg) * (FB / 4) + i];
+                        const float4 fv = (!FMA && cg == 0) ? fpre : rx[(2 + cg) * (FB / 4) + i];
                         float4 p0, p1;  // (F S^p X, (F F) S^p X) per point
                         p0.x = A::mul(fv.x, u.x);
                         p0.z = A::mul(fv.y, u.y);
