@@ -1,0 +1,83 @@
+"""Parity at BASELINE.json's full c1 size (80 x 480 x 854, kernel 5x11x11).
+
+The CPU reference can afford single steps and a short global-step loop at
+this size (all host threads), so these are direct comparisons, plus
+size-independent properties of the operator:
+  * EXACT step == reference sfseg_step, bit for bit (engine.cpp:141-166)
+  * scaling: step(2x) == 2 step(x) exactly (every product and sum scales by a
+    power of two), EXACT and FAST
+  * symmetry: the affinity matrix is symmetric (oracle.cpp:67-175), so
+    <x, M y> == <M x, y> up to fp32 rounding, EXACT and FAST
+  * the whole c1 workload (30 iterations, binarisation off) against the
+    reference's normalize_l2(sfseg_step) loop (bench.cpp:154-155), which
+    run() equals bit for bit (test_engine.cpp:276-297): north-star gates
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1907_02731_b200 import engine as E
+from paper_1907_02731_b200 import synth
+from tests.oracle_lib import Reference, random_volume, reference_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")]
+
+THREADS = max(1, os.cpu_count() or 1)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    prob = synth.config(1)[0]
+    fs, _ = prob.generate()
+    return prob, fs
+
+
+def _cfg(prob, arith, **kw):
+    return E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, **kw})
+
+
+def test_full_c1_step_bit_exact(c1):
+    prob, fs = c1
+    x = random_volume(prob.shape, 7)
+    cfg = _cfg(prob, "exact")
+    got = E.sfseg_step(x, fs, cfg)
+    want = Reference().step(x, fs.unary, fs.pairwise, cfg, threads=THREADS)
+    assert np.array_equal(got, want), f"{int(np.sum(got != want))} values differ"
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_full_c1_step_scales_exactly(c1, arith):
+    prob, fs = c1
+    x = random_volume(prob.shape, 8)
+    cfg = _cfg(prob, arith)
+    y1 = E.sfseg_step(x, fs, cfg)
+    y2 = E.sfseg_step((2.0 * x).astype(np.float32), fs, cfg)
+    assert np.array_equal(y2, 2.0 * y1)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_full_c1_operator_is_symmetric(c1, arith):
+    prob, fs = c1
+    x = random_volume(prob.shape, 9)
+    y = random_volume(prob.shape, 10)
+    cfg = _cfg(prob, arith)
+    mx = E.sfseg_step(x, fs, cfg).astype(np.float64)
+    my = E.sfseg_step(y, fs, cfg).astype(np.float64)
+    a = float(np.dot(x.astype(np.float64).ravel(), my.ravel()))
+    b = float(np.dot(y.astype(np.float64).ravel(), mx.ravel()))
+    assert abs(a - b) <= 1e-6 * abs(a), (a, b)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_full_c1_solve_matches_reference_global_loop(c1, arith):
+    prob, fs = c1
+    iters = prob.cfg.iterations  # 30
+    cfg = _cfg(prob, arith, iterations=iters, binarize_start=iters + 1)
+    res = E.run(fs, cfg)
+    want = Reference().global_loop(fs.unary, fs.pairwise, cfg, iters, threads=THREADS).astype(np.float64)
+    got = res.soft.astype(np.float64)
+    err = float(np.max(np.abs(got - want)))
+    cos = float(np.dot(got.ravel(), want.ravel()) / (np.linalg.norm(got) * np.linalg.norm(want)))
+    assert err <= 1e-4, err
+    assert cos >= 1 - 1e-6, cos
