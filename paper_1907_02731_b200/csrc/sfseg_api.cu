@@ -23,6 +23,7 @@
 #include "aux_kernels.cuh"
 #include "fused_step.cuh"
 #include "fused_ws.cuh"
+#include "fused_rs.cuh"
 
 namespace {
 
@@ -233,6 +234,34 @@ FusedVariant variant_ws() {
     return v;
 }
 
+#ifndef SFK_RS_NWA
+#define SFK_RS_NWA 8
+#endif
+#ifndef SFK_RS_STAGES
+#define SFK_RS_STAGES 3
+#endif
+// FAST: products formed in registers inside the x-pass (fused_rs.cuh)
+template <int RT, int R, int NWA = SFK_RS_NWA, int ST = SFK_RS_STAGES>
+FusedVariant variant_rs() {
+    using G = sfk::RsGeom<RT, R, NWA, ST>;
+    FusedVariant v;
+    v.rt = RT;
+    v.r = R;
+    v.ty = G::TY;
+    v.tx = G::TX;
+    v.fma = true;
+    v.smem = G::SMEM_BYTES;
+    v.threads = G::NT;
+    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, false>;
+    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, true>;
+    v.box_w = G::BW;
+    v.box_h = G::BH;
+    return v;
+}
+
+#define SFK_VARIANTS_RS() \
+    variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>()
+
 #define SFK_VARIANTS_WS(FMA_)                                                             \
     variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \
         variant_ws<2, 5, FMA_>()
@@ -241,16 +270,19 @@ FusedVariant variant_ws() {
     variant<1, 2, 48, 32, FMA_>(), variant<1, 3, 48, 32, FMA_>(),                        \
         variant<2, 4, 48, 32, FMA_>(), variant<2, 5, 48, 32, FMA_>()
 
-// SFSEG_KERNEL=v4 selects the single-role kernel (fused_step.cuh) for
-// comparison; the default is the warp-specialised one (fused_ws.cuh).
+// Default: EXACT runs the warp-specialised kernel (fused_ws.cuh), FAST the
+// register-streamed one (fused_rs.cuh). SFSEG_KERNEL=ws runs fused_ws for
+// FAST too, SFSEG_KERNEL=v4 the single-role kernel (fused_step.cuh); both
+// are kept for comparison.
 const std::vector<FusedVariant>& variants() {
-    static const bool v4 = [] {
+    static const std::string which = [] {
         const char* e = std::getenv("SFSEG_KERNEL");
-        return e && std::string(e) == "v4";
+        return std::string(e ? e : "");
     }();
+    static const std::vector<FusedVariant> rs = {SFK_VARIANTS_WS(false), SFK_VARIANTS_RS()};
     static const std::vector<FusedVariant> ws = {SFK_VARIANTS_WS(false), SFK_VARIANTS_WS(true)};
     static const std::vector<FusedVariant> old = {SFK_VARIANTS(false), SFK_VARIANTS(true)};
-    return v4 ? old : ws;
+    return which == "v4" ? old : which == "ws" ? ws : rs;
 }
 
 // Host scheduler for the persistent stencil grid: G CTAs, ntiles tiles of
