@@ -404,8 +404,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                         "kernel": f"fused_step_ws<RT={cfg.kernel.radii[0]},R={max(cfg.kernel.radii[1:])},"
-                                   f"{args.arith.upper()}>",
+                         "kernel": (f"fused_step_rs<RT={cfg.kernel.radii[0]},R={max(cfg.kernel.radii[1:])}> (FAST)"
+                                    if args.arith == "fast" else
+                                    f"fused_step_ws<RT={cfg.kernel.radii[0]},R={max(cfg.kernel.radii[1:])},EXACT>"),
                          "avg_launch_ms": avg_launch_ms, "bytes_per_launch": bytes_per_launch},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,

@@ -31,19 +31,43 @@
 
 #include "device_common.cuh"
 #include "fused_step.cuh"  // PlaneStream, Arith, ffma2
+#include "fused_ws.cuh"    // SFK_T timeline instrumentation
 #include "sfseg_types.cuh"
 
 #ifndef SFK_RS_EXP
 #define SFK_RS_EXP 0
 #endif
+// SFK_RS_TMR=1: B keeps the t-pass ring of y-filtered planes in tensor
+// memory (tcgen05.ld/st) instead of registers
+#ifndef SFK_RS_TMR
+#define SFK_RS_TMR 0
+#endif
+// SFK_RS_SPLIT=1: the B role is split in two warp groups that meet in a TMEM
+// ring: B warps run the y-pass and store each y-filtered plane into tensor
+// memory; C warps (same TMEM lane quadrants) run the t-pass from it, the
+// recombination, the store and the reductions
+#ifndef SFK_RS_SPLIT
+#define SFK_RS_SPLIT 0
+#endif
+// SFK_RS_LSU=1: B fetches the recombination operands with plain loads one
+// emitted plane ahead and stores y_{k+1} with plain stores, which leaves the
+// per-SM TMA unit to the halo boxes alone (it is the busiest unit: ~32 B/clk)
+#ifndef SFK_RS_LSU
+#define SFK_RS_LSU 0
+#endif
 
 namespace sfk {
 
-template <int RT, int R, int NWA, int STAGES>
+// TY: tile rows; BR: output rows per B thread (a B warp covers BR rows x 32
+// columns, so there are TY / BR B warps)
+template <int RT, int R, int NWA, int STAGES, int TY_ = 64, int BR_ = 8>
 struct RsGeom {
-    static constexpr int TY = 64, TX = 32;
-    static constexpr int NA = 32 * NWA, NB = 256, NT = NA + NB;
-    static constexpr int NWB = NB / 32;
+    static constexpr int TY = TY_, TX = 32, BR = BR_;
+    static constexpr bool SPLIT = SFK_RS_SPLIT != 0;
+    static constexpr int NWB = TY / BR;
+    static constexpr int NWC = SPLIT ? NWB : 0;
+    static constexpr int NA = 32 * NWA, NB = 32 * NWB, NC = 32 * NWC, NT = NA + NB + NC;
+    static constexpr int NS = 8;  // TMEM ring slots per thread (SPLIT)
     static constexpr int K = 2 * RT + 1;
     static constexpr int BH = TY + 2 * R;
     // x halos: the box must start on a 16-byte boundary (TMA faults on an
@@ -52,7 +76,11 @@ struct RsGeom {
     // number of float4s, which makes float4 reads of 8 rows at one strip
     // conflict-free
     static constexpr int HX = (R + 3) / 4 * 4;
-    static constexpr int HR = ((TX + HX + (R + 3) / 4 * 4) / 4) % 2 == 1 ? (R + 3) / 4 * 4 : (R + 3) / 4 * 4 + 4;
+#ifndef SFK_RS_ODDBOX
+#define SFK_RS_ODDBOX 1
+#endif
+    static constexpr int HR = (!SFK_RS_ODDBOX || ((TX + HX + (R + 3) / 4 * 4) / 4) % 2 == 1) ? (R + 3) / 4 * 4
+                                                                                             : (R + 3) / 4 * 4 + 4;
     static constexpr int BW = TX + HX + HR;
     static constexpr int BW4 = BW / 4;
     static constexpr int XOFF = HX - R;  // first box column a strip reads
@@ -71,73 +99,107 @@ struct RsGeom {
     static constexpr int XBUF = XBU + XBP;
     static constexpr int NBANDS = TY / 4;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
-    static constexpr size_t XB_FLOATS = 2 * size_t(XBUF);
-    static constexpr size_t SMEM_BYTES = (RAW_FLOATS + XB_FLOATS) * sizeof(float) + 256;
-    // setmaxnreg budgets: warp w runs on SMSP w % 4 and each SMSP has 512
-    // registers per lane slot; the fullest SMSP bounds the budgets
-    static constexpr int WA_MAX = (NWA + 3) / 4;            // A warps on the fullest SMSP
+#ifndef SFK_RS_NXB
+#define SFK_RS_NXB 2
+#endif
+    static constexpr int NXB = SFK_RS_NXB;  // x-pass buffers between A and B
+    static constexpr size_t XB_FLOATS = NXB * size_t(XBUF);
+    // per B warp: S^p and F of its BR output rows (TMA, loaded one emitted
+    // plane ahead) and the staging rows of y_{k+1} for the TMA store
+    static constexpr int SLAB = BR * TX;
+    static constexpr size_t SL_FLOATS = size_t(NWB) * 3 * SLAB;
+    static constexpr int NBAR = STAGES + 2 * SFK_RS_NXB + NWB + (SPLIT ? 2 * NWB * NS : 0);
+    static constexpr size_t SMEM_BYTES = (RAW_FLOATS + XB_FLOATS + SL_FLOATS) * sizeof(float) + NBAR * 8;
+    // setmaxnreg budgets. Warp w runs on SMSP w % 4, whose register file
+    // holds 512 registers per lane slot; the launch grants every warp
+    // 512 / (most warps on one SMSP), and the budgets must fit every SMSP.
 #ifndef SFK_RS_RA
 #define SFK_RS_RA 64
 #endif
     static constexpr int RA = SFK_RS_RA;
-    static constexpr int WMAX = (NWA + NWB + 3) / 4;
-    // B warps NWA..NWA+7: SMSPs hold WA_s A warps and WB_s B warps; take the
-    // tightest SMSP
+    static constexpr int NW = NWA + NWB + NWC;
+    static constexpr int RPOOL = (512 / ((NW + 3) / 4)) / 8 * 8;
+    // unsplit: the B warps take what A gives back. SPLIT: B keeps the launch
+    // grant and the C warps take what A gives back.
     static constexpr int rb_for(int s) {
-        const int wa = NWA / 4 + (s < NWA % 4 ? 1 : 0);
-        int wb = 0;
-        for (int w = NWA; w < NWA + NWB; ++w) wb += (w % 4 == s) ? 1 : 0;
-        return wb ? (512 - wa * RA) / wb : 512;
+        int wa = 0, wb = 0, wk = 0;
+        for (int w = 0; w < NW; ++w)
+            if (w % 4 == s) {
+                if (w < NWA) ++wa;
+                else if (SPLIT && w < NWA + NWB) ++wk;
+                else ++wb;
+            }
+        return wb ? (512 - wa * RA - wk * RPOOL) / wb : 512;
     }
-    static constexpr int RB_RAW = rb_for(0) < rb_for(1) ? (rb_for(0) < rb_for(2) ? (rb_for(0) < rb_for(3) ? rb_for(0) : rb_for(3)) : (rb_for(2) < rb_for(3) ? rb_for(2) : rb_for(3)))
-                                                        : (rb_for(1) < rb_for(2) ? (rb_for(1) < rb_for(3) ? rb_for(1) : rb_for(3)) : (rb_for(2) < rb_for(3) ? rb_for(2) : rb_for(3)));
-    static constexpr int RPOOL = (65536 / NT) / 8 * 8;  // launch grant per thread
-    static constexpr int RB_POOL = (NT * RPOOL - NA * RA) / NB;
-    static constexpr int RB_MIN = RB_RAW < RB_POOL ? RB_RAW : RB_POOL;
-    static constexpr int RB = (RB_MIN < 248 ? RB_MIN : 248) / 8 * 8;
-    static_assert(BW4 % 2 == 1, "odd float4 box rows");
+    static constexpr int rb_min() {
+        int m = 512;
+        for (int s = 0; s < 4; ++s) m = rb_for(s) < m ? rb_for(s) : m;
+        return m;
+    }
+    // and the CTA's launch pool: B takes no more than A gives back
+    static constexpr int RB_POOL = RPOOL + (RPOOL - RA) * NWA / (SPLIT ? NWC : NWB);
+    static constexpr int RB_CAP = rb_min() < RB_POOL ? rb_min() : RB_POOL;
+    static constexpr int RB = (RB_CAP < 248 ? RB_CAP : 248) / 8 * 8;
+    static_assert(BW4 % 2 == 1 || !SFK_RS_ODDBOX, "odd float4 box rows");
     static_assert((TXU / 4) % 2 == 1 && (TXQ / 4) % 2 == 1, "conflict-free x-pass rows");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
     static_assert(RA <= RPOOL && RB >= RPOOL, "setmaxnreg: A gives, B takes");
+    static_assert(NWA % 4 == 0 && NWB % 4 == 0, "setmaxnreg acts on whole warpgroups");
+    static_assert(!SPLIT || (BR == 8 && NS * 3 * BR <= 256), "SPLIT: TMEM ring of one thread");
+    static_assert(TY % BR == 0 && (BR == 4 || BR == 8), "B rows per thread");
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
-template <int RT, int R, int NWA, int STAGES, bool ACC>
-__global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_constant__ FusedArgs a) {
-    using G = RsGeom<RT, R, NWA, STAGES>;
+template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool ACC>
+__global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
+    fused_step_rs(const __grid_constant__ FusedArgs a) {
+    using G = RsGeom<RT, R, NWA, STAGES, TY_, BR_>;
     using A = Arith<true>;
-    constexpr int TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K;
-    constexpr int BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4;
-    constexpr int TXU = G::TXU, TXQ = G::TXQ, XBU = G::XBU, XBUF = G::XBUF;
+    constexpr int BR = G::BR, TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K, NWB = G::NWB;
+    constexpr int BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4, SW = G::SW;
+    constexpr int TXU = G::TXU, TXQ = G::TXQ, XBU = G::XBU, XBUF = G::XBUF, SLAB = G::SLAB;
 
     extern __shared__ __align__(128) float smem[];
-    float* raw = smem;                   // [STAGES][3][FB]   TMA boxes
-    float* xb = raw + G::RAW_FLOATS;     // [2][XBUF]         x-pass output
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(xb + G::XB_FLOATS);
-    uint64_t* raw_full = mbar;               // [STAGES]  TMA -> A
-    uint64_t* xb_full = mbar + STAGES;       // [2]       A -> B (count NA)
-    uint64_t* xb_empty = mbar + STAGES + 2;  // [2]       B -> A (count NB)
+    float* raw = smem;                    // [STAGES][3][FB]    TMA boxes
+    constexpr int NXB = G::NXB;
+    float* xb = raw + G::RAW_FLOATS;      // [NXB][XBUF]        x-pass output
+    float* bsl = xb + G::XB_FLOATS;       // [NWB][3][BR][TX]   S^p, F, y_{k+1} rows
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(bsl + G::SL_FLOATS);
+    uint64_t* raw_full = mbar;                // [STAGES]  TMA -> A
+    uint64_t* xb_full = mbar + STAGES;              // [NXB]  A -> B (count NA)
+    uint64_t* xb_empty = mbar + STAGES + NXB;       // [NXB]  B -> A (count NB)
+    uint64_t* slab_full = mbar + STAGES + 2 * NXB;  // [NWB]  TMA -> B (C) warp
+    uint64_t* ring_full = slab_full + NWB;          // [NWB][NS]  B -> C (SPLIT)
+    uint64_t* ring_free = ring_full + NWB * G::NS;  // [NWB][NS]  C -> B (SPLIT)
 
     __shared__ IterState st;
     __shared__ PlaneStream prodq;
+    __shared__ PlaneStream slabq[NWB];
     __shared__ int prod_count;
+    __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
-    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    if (a.st->degenerate && SFK_RS_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;
 
     if (tid == 0) {
         st = *a.st;
         for (int s = 0; s < STAGES; ++s) mbar_init(&raw_full[s], 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NXB; ++b) {
             mbar_init(&xb_full[b], NA);
             mbar_init(&xb_empty[b], NB);
         }
+        for (int w = 0; w < NWB; ++w) mbar_init(&slab_full[w], 1);
+        if constexpr (G::SPLIT)
+            for (int w = 0; w < 2 * NWB * G::NS; ++w) mbar_init(&ring_full[w], 32);
         fence_barrier_init();
         prefetch_tensormap(&a.tm_x);
         prefetch_tensormap(&a.tm_sp);
         prefetch_tensormap(&a.tm_f[0]);
+        prefetch_tensormap(&a.tm_out);
+        prefetch_tensormap(&a.tm_spc);
+        prefetch_tensormap(&a.tm_fc[0]);
     }
     __syncthreads();
 
@@ -175,12 +237,14 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
         const bool sigm = st.mode == 2;
         const int xw = tid >> 5, xl = tid & 31;  // warp; lane -> (row xl & 7, strip xl >> 3)
 
-        // one x-pass item: row r, strip sx; SIG applies the sigmoid to y_k
+        // one x-pass item (conv3d.cpp:88-101): row r, strip sx (SW outputs).
+        // u runs as column pairs (2k, 2k+1) with tap pairs (w[e], w[e-1]);
+        // (F u, F^2 u) runs as a pair per column with a broadcast tap.
         auto item = [&](auto sig_c, const float* rs, float* xbu, float* xbp, int r, int sx) {
             constexpr bool SIG = decltype(sig_c)::value;
             const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + 2 * sx;
-            float ou[G::SW];
-            float2 op[G::SW];
+            float2 ou[SW / 2];
+            float2 op[SW];
             float4 yv, sv, fv;
 #pragma unroll
             for (int m4 = 0; m4 < G::NLD * 4; ++m4) {
@@ -200,25 +264,25 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
                 const float fu = f * u;
                 const float2 pr = make_float2(fu, f * fu);
 #pragma unroll
-                for (int j = 0; j < G::SW; ++j) {
+                for (int k = 0; k < SW / 2; ++k) {
+                    const int e = m - 2 * k;
+                    if (e < 0 || e > 2 * R + 1) continue;
+                    ou[k] = ffma2(make_float2(u, u), a.tpair_x[e], e == 0 ? zero2 : ou[k]);
+                }
+#pragma unroll
+                for (int j = 0; j < SW; ++j) {
                     const int d = m - j;
                     if (d < 0 || d > 2 * R) continue;
-                    if (d == 0) {
-                        ou[j] = a.taps_x[0] * u;
-                        op[j] = ffma2(pr, make_float2(a.taps_x[0], a.taps_x[0]), zero2);
-                    } else {
-                        ou[j] = fmaf(a.taps_x[d], u, ou[j]);
-                        op[j] = ffma2(pr, make_float2(a.taps_x[d], a.taps_x[d]), op[j]);
-                    }
+                    op[j] = ffma2(pr, make_float2(a.taps_x[d], a.taps_x[d]), d == 0 ? zero2 : op[j]);
                 }
             }
-            float4* du = reinterpret_cast<float4*>(xbu + r * TXU + sx * G::SW);
+            float4* du = reinterpret_cast<float4*>(xbu + r * TXU + sx * SW);
 #pragma unroll
-            for (int v = 0; v < G::SW / 4; ++v)
-                du[v] = make_float4(ou[4 * v], ou[4 * v + 1], ou[4 * v + 2], ou[4 * v + 3]);
-            float4* dp = reinterpret_cast<float4*>(xbp + r * TXQ + 2 * sx * G::SW);
+            for (int v = 0; v < SW / 4; ++v)
+                du[v] = make_float4(ou[2 * v].x, ou[2 * v].y, ou[2 * v + 1].x, ou[2 * v + 1].y);
+            float4* dp = reinterpret_cast<float4*>(xbp + r * TXQ + 2 * sx * SW);
 #pragma unroll
-            for (int v = 0; v < G::SW / 2; ++v)
+            for (int v = 0; v < SW / 2; ++v)
                 dp[v] = make_float4(op[2 * v].x, op[2 * v].y, op[2 * v + 1].x, op[2 * v + 1].y);
         };
 
@@ -229,9 +293,12 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
             const int tg = a.out_t0 + q.p;
             if (tg < 0 || tg >= a.T) continue;  // planes outside the volume: B zero-fills
             const int s = cnt % STAGES;
-            const int b = cnt & 1;
+            const int b = cnt % NXB;
+            if (tid == 0 || tid == 64) SFK_T(cnt, tid ? 13 : 0);
             mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
-            mbar_wait(&xb_empty[b], ((cnt >> 1) & 1) ^ 1);
+            if (tid == 0) SFK_T(cnt, 1);
+            mbar_wait(&xb_empty[b], ((cnt / NXB) & 1) ^ 1);
+            if (tid == 0) SFK_T(cnt, 2);
             const float* rs = raw + static_cast<size_t>(s) * 3 * FB;
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
@@ -246,21 +313,223 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
                 else
                     item(std::false_type{}, rs, xbu, xbp, r, xl >> 3);
             }
+            if (tid == 0 || tid == 64) SFK_T(cnt, tid ? 14 : 3);
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
+            if (tid == 0) SFK_T(cnt, 4);
             if (tid == 0) {
                 fence_proxy_async();  // generic reads of stage s before the TMA overwrite
                 issue_next();
             }
             ++cnt;
         }
+    } else if constexpr (G::SPLIT) {
+        // =====================================================================
+        // SPLIT: B = y-pass into a TMEM ring; C = t-pass, recombination,
+        // store, reductions. B warp i and C warp i share a TMEM lane quadrant.
+        // =====================================================================
+        constexpr int NS = G::NS, RW = 3 * BR;
+        const int bt = tid - NA;
+        const bool isC = bt >= NB;
+        const int wi = (isC ? bt - NB : bt) >> 5;
+        const int lane = bt & 31;
+        if (bt < 32) tmem_alloc<512>(&tmem_base_sh);
+        tcgen05_fence_before();
+        named_bar_sync(2, NB + G::NC);
+        tcgen05_fence_after();
+        const int wq = (NA / 32 + (bt >> 5)) & 3;  // CTA warp id % 4 (same for B warp i and C warp i)
+        const uint32_t ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) + static_cast<uint32_t>((wi >> 2) * 256);
+        uint64_t* rfull = ring_full + wi * NS;
+        uint64_t* rfree = ring_free + wi * NS;
+        if (!isC) {
+            // ---------------- B: y-pass (conv3d.cpp:113-135) ----------------
+            PlaneStream q;
+            q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            int cnt = 0;  // in-volume planes consumed
+            for (int c = 0; !q.done; q.next(), ++c) {
+                const int tg = a.out_t0 + q.p;
+                float2 au[BR / 2], ap[BR];
+#pragma unroll
+                for (int k = 0; k < BR / 2; ++k) au[k] = zero2;
+#pragma unroll
+                for (int r = 0; r < BR; ++r) ap[r] = zero2;
+                if (tg >= 0 && tg < a.T) {
+                    const int b = cnt % NXB;
+                    mbar_wait(&xb_full[b], (cnt / NXB) & 1);
+                    const float* xbu = xb + b * XBUF + (BR * wi) * TXU + lane;
+                    const float2* xbp = reinterpret_cast<const float2*>(xb + b * XBUF + XBU + (BR * wi) * TXQ) + lane;
+#pragma unroll
+                    for (int j = 0; j < BR + 2 * R; ++j) {
+                        const float vin = xbu[j * TXU];
+                        const float2 pv = xbp[j * (TXQ / 2)];
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k) {
+                            const int e = j - 2 * k;
+                            if (e < 0 || e > 2 * R + 1) continue;
+                            au[k] = ffma2(make_float2(vin, vin), a.tpair_y[e], au[k]);
+                        }
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) {
+                            const int d = j - r;
+                            if (d < 0 || d > 2 * R) continue;
+                            ap[r] = ffma2(pv, make_float2(a.taps_y[d], a.taps_y[d]), ap[r]);
+                        }
+                    }
+                    mbar_arrive(&xb_empty[b]);
+                    ++cnt;
+                }
+                const int sl = c % NS;
+                mbar_wait(&rfree[sl], ((c / NS) & 1) ^ 1);
+                tcgen05_fence_after();
+                float w[8];
+#pragma unroll
+                for (int k = 0; k < BR / 2; ++k) {
+                    w[2 * k] = au[k].x;
+                    w[2 * k + 1] = au[k].y;
+                }
+                tmem_st8(ring + sl * RW, w);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        w[2 * r] = ap[4 * h + r].x;
+                        w[2 * r + 1] = ap[4 * h + r].y;
+                    }
+                    tmem_st8(ring + sl * RW + 8 + 8 * h, w);
+                }
+                tmem_wait_st();
+                tcgen05_fence_before();
+                mbar_arrive(&rfull[sl]);
+            }
+        } else {
+            // ---------------- C: t-pass, recombination, store, reductions ----------------
+            setmaxnreg_inc<G::RB>();
+            const float inv_alpha = a.inv_alpha;
+            const bool last = a.last_group;
+            const float scale = st.mode == 1 ? st.inv_f : 1.0f;
+            float* slab = bsl + wi * 3 * SLAB;
+            uint64_t* sfull = &slab_full[wi];
+            PlaneStream& eq = slabq[wi];  // lane 0 only
+            auto issue_slab = [&]() {
+                if (eq.done) return;
+                mbar_arrive_expect_tx(sfull, 2 * SLAB * sizeof(float));
+                const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wi, t = a.out_t0 + eq.p - a.buf_t0;
+                tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
+                tma_load_3d(slab + SLAB, &a.tm_fc[0], sfull, x, y, t);
+                eq.next();
+            };
+            if (lane == 0) {
+                eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+                issue_slab();
+            }
+            PlaneStream q;
+            q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            int ecnt = 0;
+            for (int c = 0; !q.done; ++c) {
+                const bool emit = q.p - RT >= q.ta;
+                const bool seg_last = q.p + 1 >= q.tb + RT;
+                const int to = a.out_t0 + q.p - RT;
+                mbar_wait(&rfull[c % NS], (c / NS) & 1);
+                tcgen05_fence_after();
+                if (emit) {
+                    // t-pass (conv3d.cpp:147-165): planes c - 2RT .. c take taps_t[0..2RT]
+                    float2 tu[BR / 2], tp[BR];
+#pragma unroll
+                    for (int d = 0; d < K; ++d) {
+                        float wv[3][8];
+                        const int sl = (c - 2 * RT + d) % NS;
+                        tmem_ld8(ring + sl * RW, wv[0]);
+                        tmem_ld8(ring + sl * RW + 8, wv[1]);
+                        tmem_ld8(ring + sl * RW + 16, wv[2]);
+                        tmem_wait_ld();
+                        const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k)
+                            tu[k] = ffma2(make_float2(wv[0][2 * k], wv[0][2 * k + 1]), w2, d == 0 ? zero2 : tu[k]);
+#pragma unroll
+                        for (int r = 0; r < BR; ++r)
+                            tp[r] = ffma2(make_float2(wv[1 + r / 4][2 * (r % 4)], wv[1 + r / 4][2 * (r % 4) + 1]), w2,
+                                          d == 0 ? zero2 : tp[r]);
+                    }
+                    mbar_wait(sfull, ecnt & 1);
+                    float spv[BR], fv[BR];
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        spv[r] = slab[r * TX + lane];
+                        fv[r] = slab[SLAB + r * TX + lane];
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        fence_proxy_async();
+                        issue_slab();
+                    }
+                    float v[BR];
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        const float tur = (r & 1) ? tu[r / 2].y : tu[r / 2].x;
+                        v[r] = A::recombine(spv[r] * scale, fv[r], inv_alpha, tur, tp[r].y, tp[r].x);
+                    }
+                    const int ox = q.tile_x * TX, oy = q.tile_y * TY + BR * wi;
+                    if constexpr (ACC) {
+                        const int nr = a.H - oy;
+                        const float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * a.pitch + ox + lane;
+#pragma unroll
+                        for (int r = 0; r < BR; ++r)
+                            if (r < nr && ox + lane < a.W) v[r] += po[static_cast<size_t>(r) * a.pitch];
+                    }
+                    float* ost = slab + 2 * SLAB;
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) ost[r * TX + lane] = v[r];
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&a.tm_out, ost, ox, oy, to - a.out_buf_t0);
+                        bulk_commit();
+                    }
+                    ++ecnt;
+                    if (last) {
+#pragma unroll
+                        for (int h = 0; h < BR / 4; ++h) {
+                            float cs = 0.0f;
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
+#pragma unroll
+                            for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+                            const int gb = q.tile_y * G::NBANDS + (BR / 4) * wi + h;
+                            if (lane == 0 && gb < a.nbands && q.tile_x < a.nhalves)
+                                a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
+                                    static_cast<double>(cs);
+                        }
+                        float cmax = 0.0f;
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
+                        const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                        if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
+                    }
+                }
+                // release the ring slots no future output of this segment needs
+                tcgen05_fence_before();
+                if (emit) mbar_arrive(&rfree[(c - 2 * RT) % NS]);
+                if (seg_last)
+                    for (int d = 2 * RT - 1; d >= 0; --d) mbar_arrive(&rfree[(c - d) % NS]);
+                q.next();
+            }
+            if (lane == 0) bulk_wait0();
+        }
+        tcgen05_fence_before();
+        named_bar_sync(2, NB + G::NC);
+        tcgen05_fence_after();
+        if (bt < 32) tmem_dealloc<512>(tmem_base_sh);
     } else {
         // =====================================================================
         // B: y-pass ring, t-pass, recombination (x 1/||y_k||), store, reductions
         // =====================================================================
         setmaxnreg_inc<G::RB>();
         const int bt = tid - NA;
-        // B thread = one column (its lane) x 8 rows (8 wb .. 8 wb + 7) of the tile
+        // B thread = one column (its lane) x BR rows (BR wb .. BR wb + BR - 1);
+        // u runs as row pairs (2k, 2k+1), (F u, F^2 u) as a pair per row
         const int lane = bt & 31;
         const int wb = bt >> 5;
         const float inv_alpha = a.inv_alpha;
@@ -269,55 +538,102 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
         // sigmoid iterations (mode 2) normalised on load, iteration 1 has none
         const float scale = st.mode == 1 ? st.inv_f : 1.0f;
 
-        float ringu[8][K];       // u
-        float2 ringp[8][K];      // (F u, F^2 u)
+        constexpr bool TMR = SFK_RS_TMR != 0;
+        constexpr int KR = TMR ? 1 : K;  // register ring depth
+        float2 ringu[BR / 2][KR];  // u of rows (2k, 2k+1)
+        float2 ringp[BR][KR];      // (F u, F^2 u) of row r
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int k = 0; k < KR; ++k) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                ringu[r][k] = 0.0f;
-                ringp[r][k] = zero2;
+            for (int r = 0; r < BR / 2; ++r) ringu[r][k] = zero2;
+#pragma unroll
+            for (int r = 0; r < BR; ++r) ringp[r][k] = zero2;
+        }
+        // TMEM ring (TMR): slot = 3 BR words (u pairs, then (F u, F^2 u) per
+        // row) in this thread's TMEM lane; warps w and w + 4 share a lane
+        // quadrant and take the two column halves
+        constexpr int RW = 3 * BR;
+        static_assert(!TMR || (BR == 8 && K * RW <= 128), "TMEM ring of one thread");
+        uint32_t tm_ring = 0;
+        if constexpr (TMR) {
+            if (wb == 0) tmem_alloc<256>(&tmem_base_sh);
+            tcgen05_fence_before();
+            named_bar_sync(2, NB);
+            tcgen05_fence_after();
+            const int wq = (NWA + wb) & 3;  // CTA warp id % 4
+            tm_ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) + static_cast<uint32_t>((wb >> 2) * 128);
+        }
+        auto ring_ld = [&](int slot, float2 (&lu)[BR / 2], float2 (&lp)[BR]) {
+            float w[3][8];
+            tmem_ld8(tm_ring + slot * RW, w[0]);
+            tmem_ld8(tm_ring + slot * RW + 8, w[1]);
+            tmem_ld8(tm_ring + slot * RW + 16, w[2]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < BR / 2; ++k) lu[k] = make_float2(w[0][2 * k], w[0][2 * k + 1]);
+#pragma unroll
+            for (int r = 0; r < BR; ++r) lp[r] = make_float2(w[1 + r / 4][2 * (r % 4)], w[1 + r / 4][2 * (r % 4) + 1]);
+        };
+
+        // recombination operands S^p, F of this warp's BR rows: TMA, one
+        // emitted plane ahead (cursor eq walks the output planes in schedule
+        // order); zero-filled outside the volume, so those points come out as
+        // exactly 0, add nothing to the sums, and the TMA store clips them
+        float* slab = bsl + wb * 3 * SLAB;
+        uint64_t* sfull = &slab_full[wb];
+        PlaneStream& eq = slabq[wb];  // lane 0 only
+        auto issue_slab = [&]() {
+            if (eq.done) return;
+            mbar_arrive_expect_tx(sfull, 2 * SLAB * sizeof(float));
+            const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
+            tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
+            tma_load_3d(slab + SLAB, &a.tm_fc[0], sfull, x, y, t);
+            eq.next();
+        };
+        constexpr bool LSU = SFK_RS_LSU != 0;
+        if (lane == 0 && !(SFK_RS_EXP & 16) && !LSU) {
+            eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+            issue_slab();
+        }
+        // LSU: operands of the next emitted plane in registers; one 64-bit
+        // base per plane, then row increments; rows past H are predicated off
+        // and columns past W read / write the pitch padding (S^p is 0 there)
+        float nsp[BR], nf[BR];
+        PlaneStream lq;
+        const size_t rowstep = static_cast<size_t>(a.pitch);
+        auto fetch = [&]() {
+#pragma unroll
+            for (int r = 0; r < BR; ++r) {
+                nsp[r] = 0.0f;
+                nf[r] = 0.0f;
             }
+            if (lq.done) return;
+            const int y0 = lq.tile_y * TY + BR * wb, nr = a.H - y0;
+            const size_t off = (static_cast<size_t>(a.out_t0 + lq.p - a.buf_t0) * a.H + y0) * rowstep +
+                               lq.tile_x * TX + lane;
+            const float* ps = a.sp + off;
+            const float* pf = a.f[0] + off;
+#pragma unroll
+            for (int r = 0; r < BR; ++r)
+                if (r < nr) {
+                    nsp[r] = __ldg(ps + r * rowstep);
+                    nf[r] = __ldg(pf + r * rowstep);
+                }
+            lq.next();
+        };
+        if constexpr (LSU) {
+            lq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+            fetch();
+        }
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
         int cnt = 0;   // in-volume planes consumed
-        // recombination operands S^p, F of this thread's 8 output points,
-        // loaded one emitted plane ahead (cursor eq walks the output planes in
-        // schedule order); rows / columns outside the volume read as 0, so
-        // those points come out as exactly 0 and add nothing to the sums
-        float nsp[8], nf[8];
-        PlaneStream eq;
-        eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
-        auto fetch = [&]() {
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                nsp[r] = 0.0f;
-                nf[r] = 0.0f;
-            }
-            if (eq.done) return;
-            // one 64-bit address per plane, then row increments; rows past H
-            // are predicated off (columns past W read the zero pitch padding)
-            const int y0 = eq.tile_y * TY + 8 * wb, nr = a.H - y0;
-            const size_t off = (static_cast<size_t>(a.out_t0 + eq.p - a.buf_t0) * a.H + y0) * a.pitch +
-                               eq.tile_x * TX + lane;
-            const float* ps = a.sp + off;
-            const float* pf = a.f[0] + off;
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                if (r < nr) {
-                    nsp[r] = __ldg(ps);
-                    nf[r] = __ldg(pf);
-                }
-                ps += a.pitch;
-                pf += a.pitch;
-            }
-            eq.next();
-        };
-        fetch();
+        int ecnt = 0;  // output planes emitted
 
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
+            constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const bool emit = q.p - RT >= q.ta;
@@ -325,85 +641,201 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
 
             // y-pass (conv3d.cpp:113-135) into this plane's ring slot
             if (valid) {
-                const int b = cnt & 1;
-                mbar_wait(&xb_full[b], (cnt >> 1) & 1);
-                const float* xbu = xb + b * XBUF + (8 * wb) * TXU + lane;
-                const float2* xbp = reinterpret_cast<const float2*>(xb + b * XBUF + XBU + (8 * wb) * TXQ) + lane;
+                const int b = cnt % NXB;
+                if (bt == 0) SFK_T(cnt, 6);
+                mbar_wait(&xb_full[b], (cnt / NXB) & 1);
+                if (bt == 0) SFK_T(cnt, 7);
+                const float* xbu = xb + b * XBUF + (BR * wb) * TXU + lane;
+                const float2* xbp = reinterpret_cast<const float2*>(xb + b * XBUF + XBU + (BR * wb) * TXQ) + lane;
+                if constexpr (TMR) {
+                    // all BR + 2R input rows in registers first, then tap-major
+                    // order: consecutive FFMA2s feed different accumulators
+                    float vin[BR + 2 * R];
+                    float2 pv[BR + 2 * R];
 #pragma unroll
-                for (int j = 0; j < ((SFK_RS_EXP & 2) ? 0 : 8 + 2 * R); ++j) {
+                    for (int j = 0; j < BR + 2 * R; ++j) {
+                        vin[j] = xbu[j * TXU];
+                        pv[j] = xbp[j * (TXQ / 2)];
+                    }
+#pragma unroll
+                    for (int e = 0; e <= 2 * R + 1; ++e) {
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k)
+                            ringu[k][0] = ffma2(make_float2(vin[2 * k + e], vin[2 * k + e]), a.tpair_y[e],
+                                                e == 0 ? zero2 : ringu[k][0]);
+                        if (e <= 2 * R) {
+#pragma unroll
+                            for (int r = 0; r < BR; ++r)
+                                ringp[r][0] = ffma2(pv[r + e], make_float2(a.taps_y[e], a.taps_y[e]),
+                                                    e == 0 ? zero2 : ringp[r][0]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                for (int j = 0; j < ((SFK_RS_EXP & 2) ? 0 : BR + 2 * R); ++j) {
                     const float vin = xbu[j * TXU];
                     const float2 pv = xbp[j * (TXQ / 2)];
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
+                    for (int k = 0; k < BR / 2; ++k) {
+                        const int e = j - 2 * k;
+                        if (e < 0 || e > 2 * R + 1) continue;
+                        ringu[k][SR] = ffma2(make_float2(vin, vin), a.tpair_y[e], e == 0 ? zero2 : ringu[k][SR]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
                         const int d = j - r;
                         if (d < 0 || d > 2 * R) continue;
-                        if (d == 0) {
-                            ringu[r][S_] = a.taps_y[0] * vin;
-                            ringp[r][S_] = ffma2(pv, make_float2(a.taps_y[0], a.taps_y[0]), zero2);
-                        } else {
-                            ringu[r][S_] = fmaf(a.taps_y[d], vin, ringu[r][S_]);
-                            ringp[r][S_] = ffma2(pv, make_float2(a.taps_y[d], a.taps_y[d]), ringp[r][S_]);
-                        }
+                        ringp[r][SR] = ffma2(pv, make_float2(a.taps_y[d], a.taps_y[d]), d == 0 ? zero2 : ringp[r][SR]);
                     }
                 }
+                }
+                if (bt == 0) SFK_T(cnt, 8);
                 mbar_arrive(&xb_empty[b]);
                 ++cnt;
             } else {
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    ringu[r][S_] = 0.0f;
-                    ringp[r][S_] = zero2;
-                }
+                for (int r = 0; r < BR / 2; ++r) ringu[r][SR] = zero2;
+#pragma unroll
+                for (int r = 0; r < BR; ++r) ringp[r][SR] = zero2;
             }
-            if (emit) {
-                // columns past W land in the pitch padding as exact zeros (S^p
-                // is 0 there); rows past H are predicated off
-                const int y0 = q.tile_y * TY + 8 * wb, nr = a.H - y0;
-                float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + y0) * a.pitch +
-                            q.tile_x * TX + lane;
-                float v[8];
+            if (emit && !(SFK_RS_EXP & 8)) {
+                // t-pass (conv3d.cpp:147-165): oldest..newest take taps_t[0..2RT]
+                float2 tu[BR / 2], tp[BR];
+                if constexpr (TMR) {
+                    // planes oldest..newest: K - 1 TMEM slots, then this plane
+                    tmem_wait_st();
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    // t-pass (conv3d.cpp:147-165): oldest..newest take taps_t[0..2RT]
-                    float tu = a.taps_t[0] * ringu[r][(S_ + 1) % K];
-                    float2 tp = ffma2(ringp[r][(S_ + 1) % K], make_float2(a.taps_t[0], a.taps_t[0]), zero2);
+                    for (int d = 0; d < K; ++d) {
+                        float2 lu[BR / 2], lp[BR];
+                        if (d == K - 1) {
 #pragma unroll
-                    for (int d = 1; d < K; ++d) {
-                        tu = fmaf(a.taps_t[d], ringu[r][(S_ + 1 + d) % K], tu);
-                        tp = ffma2(ringp[r][(S_ + 1 + d) % K], make_float2(a.taps_t[d], a.taps_t[d]), tp);
+                            for (int k = 0; k < BR / 2; ++k) lu[k] = ringu[k][0];
+#pragma unroll
+                            for (int r = 0; r < BR; ++r) lp[r] = ringp[r][0];
+                        } else {
+                            ring_ld((S_ + 1 + d) % K, lu, lp);
+                        }
+                        const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k) tu[k] = ffma2(lu[k], w2, d == 0 ? zero2 : tu[k]);
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) tp[r] = ffma2(lp[r], w2, d == 0 ? zero2 : tp[r]);
                     }
-                    // engine.cpp:113-119; channel sum engine.cpp:157-162
-                    const float term = A::recombine(nsp[r] * scale, nf[r], inv_alpha, tu, tp.y, tp.x);
-                    if constexpr (ACC)  // y so far (earlier groups)
-                        v[r] = r < nr ? *po + term : 0.0f;
-                    else
-                        v[r] = term;
-                    if (r < nr) *po = v[r];
-                    po += a.pitch;
-                }
-                fetch();  // the next emitted plane's operands
-                if (last) {
-                    // canonical reduction (device_common.cuh): two 4-row blocks per
-                    // warp, one column per lane, fp32 within a block (FAST)
-                    double sum[2];
+                } else {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int k = 0; k < BR / 2; ++k) {
+                        tu[k] = ffma2(ringu[k][(S_ + 1) % K], make_float2(a.taps_t[0], a.taps_t[0]), zero2);
+#pragma unroll
+                        for (int d = 1; d < K; ++d)
+                            tu[k] = ffma2(ringu[k][(S_ + 1 + d) % K], make_float2(a.taps_t[d], a.taps_t[d]), tu[k]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        tp[r] = ffma2(ringp[r][(S_ + 1) % K], make_float2(a.taps_t[0], a.taps_t[0]), zero2);
+#pragma unroll
+                        for (int d = 1; d < K; ++d)
+                            tp[r] = ffma2(ringp[r][(S_ + 1 + d) % K], make_float2(a.taps_t[d], a.taps_t[d]), tp[r]);
+                    }
+                }
+                if (bt == 0) SFK_T(ecnt, 9);
+                float spv[BR], fv[BR];
+                if constexpr (LSU) {
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        spv[r] = nsp[r];
+                        fv[r] = nf[r];
+                    }
+                    fetch();  // the next emitted plane's operands
+                } else {
+                    if (!(SFK_RS_EXP & 16)) mbar_wait(sfull, ecnt & 1);
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        spv[r] = slab[r * TX + lane];
+                        fv[r] = slab[SLAB + r * TX + lane];
+                    }
+                    __syncwarp();
+                    if (lane == 0 && !(SFK_RS_EXP & 16)) {
+                        fence_proxy_async();  // the reads above before the next TMA write
+                        issue_slab();
+                    }
+                }
+                if (bt == 0) SFK_T(ecnt, 10);
+                float v[BR];
+#pragma unroll
+                for (int r = 0; r < BR; ++r) {
+                    const float tur = (r & 1) ? tu[r / 2].y : tu[r / 2].x;
+                    // engine.cpp:113-119; channel sum engine.cpp:157-162
+                    v[r] = A::recombine(spv[r] * scale, fv[r], inv_alpha, tur, tp[r].y, tp[r].x);
+                }
+                const int ox = q.tile_x * TX, oy = q.tile_y * TY + BR * wb;
+                if constexpr (ACC) {  // y so far (earlier groups); rows past H read nothing
+                    const int nr = a.H - oy;
+                    const float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * a.pitch + ox + lane;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r)
+                        if (r < nr && ox + lane < a.W) v[r] += po[static_cast<size_t>(r) * a.pitch];
+                }
+                if constexpr (LSU) {
+                    const int nr = a.H - oy;
+                    float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * rowstep + ox + lane;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r)
+                        if (r < nr) po[r * rowstep] = v[r];
+                } else {
+                    // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
+                    float* ost = slab + 2 * SLAB;
+                    if (lane == 0) bulk_wait_read0();  // the previous store has read the staging
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) ost[r * TX + lane] = v[r];
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0 && !(SFK_RS_EXP & 16)) {
+                        tma_store_3d(&a.tm_out, ost, ox, oy, to - a.out_buf_t0);
+                        bulk_commit();
+                    }
+                }
+                if (bt == 0) SFK_T(ecnt, 11);
+                ++ecnt;
+                if (last) {
+                    // canonical reduction (device_common.cuh): BR / 4 blocks of
+                    // 4 rows per warp, one column per lane, fp32 within a block
+#pragma unroll
+                    for (int h = 0; h < BR / 4; ++h) {
                         float cs = 0.0f;
 #pragma unroll
                         for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
 #pragma unroll
                         for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-                        sum[h] = static_cast<double>(cs);
+                        const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + h;
+                        if (lane == 0 && gb < a.nbands && q.tile_x < a.nhalves)
+                            a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
+                                static_cast<double>(cs);
                     }
                     float cmax = 0.0f;
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) cmax = fmaxf(cmax, v[r]);
+                    for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
                     const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
-                    const int gb = q.tile_y * G::NBANDS + 2 * wb;
-                    if (lane < 2 && gb + lane < a.nbands && q.tile_x < a.nhalves)
-                        a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb + lane) * a.nhalves +
-                               q.tile_x] = lane ? sum[1] : sum[0];
                     if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
+                }
+            }
+            if constexpr (TMR) {
+                // this plane into slot S_ (it held a plane no longer needed)
+                float w[8];
+#pragma unroll
+                for (int k = 0; k < BR / 2; ++k) {
+                    w[2 * k] = ringu[k][0].x;
+                    w[2 * k + 1] = ringu[k][0].y;
+                }
+                tmem_st8(tm_ring + S_ * RW, w);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        w[2 * r] = ringp[4 * h + r][0].x;
+                        w[2 * r + 1] = ringp[4 * h + r][0].y;
+                    }
+                    tmem_st8(tm_ring + S_ * RW + 8 + 8 * h, w);
                 }
             }
             q.next();
@@ -417,6 +849,14 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_rs(const __grid_
             if constexpr (K > 4) { if (q.done) break; plane(integral_constant<int, (K > 4 ? 4 : 0)>{}); }
             if constexpr (K > 5) { if (q.done) break; plane(integral_constant<int, (K > 5 ? 5 : 0)>{}); }
             if constexpr (K > 6) { if (q.done) break; plane(integral_constant<int, (K > 6 ? 6 : 0)>{}); }
+        }
+        if (lane == 0) bulk_wait0();  // the output rows are written before the CTA exits
+        if constexpr (TMR) {
+            tmem_wait_st();
+            tcgen05_fence_before();
+            named_bar_sync(2, NB);
+            tcgen05_fence_after();
+            if (wb == 0) tmem_dealloc<256>(tmem_base_sh);
         }
     }
 }

@@ -240,10 +240,17 @@ FusedVariant variant_ws() {
 #ifndef SFK_RS_STAGES
 #define SFK_RS_STAGES 3
 #endif
+#ifndef SFK_RS_TY
+#define SFK_RS_TY 64
+#endif
+#ifndef SFK_RS_BR
+#define SFK_RS_BR 8
+#endif
 // FAST: products formed in registers inside the x-pass (fused_rs.cuh)
-template <int RT, int R, int NWA = SFK_RS_NWA, int ST = SFK_RS_STAGES>
+template <int RT, int R, int NWA = SFK_RS_NWA, int ST = SFK_RS_STAGES, int TY = SFK_RS_TY,
+          int BR = SFK_RS_BR>
 FusedVariant variant_rs() {
-    using G = sfk::RsGeom<RT, R, NWA, ST>;
+    using G = sfk::RsGeom<RT, R, NWA, ST, TY, BR>;
     FusedVariant v;
     v.rt = RT;
     v.r = R;
@@ -252,8 +259,8 @@ FusedVariant variant_rs() {
     v.fma = true;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, false>;
-    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, true>;
+    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, false>;
+    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
@@ -628,6 +635,12 @@ void fill_taps(FusedArgs& a, const HostKernel& k, const FusedVariant& v) {
     for (int i = 0; i <= 2 * k.rx; ++i) a.taps_x[v.r - k.rx + i] = static_cast<float>(k.x[i]);
     for (int i = 0; i <= 2 * k.ry; ++i) a.taps_y[v.r - k.ry + i] = static_cast<float>(k.y[i]);
     for (int i = 0; i <= 2 * k.rt; ++i) a.taps_t[v.rt - k.rt + i] = static_cast<float>(k.t[i]);
+    for (int e = 0; e <= 2 * v.r + 1 && e <= sfk::kMaxTapsXY; ++e) {
+        const float x0 = e <= 2 * v.r ? a.taps_x[e] : 0.0f, x1 = e >= 1 ? a.taps_x[e - 1] : 0.0f;
+        const float y0 = e <= 2 * v.r ? a.taps_y[e] : 0.0f, y1 = e >= 1 ? a.taps_y[e - 1] : 0.0f;
+        a.tpair_x[e] = make_float2(x0, x1);
+        a.tpair_y[e] = make_float2(y0, y1);
+    }
 }
 
 float* tmp_vol(sfseg_ctx* c, size_t i) {

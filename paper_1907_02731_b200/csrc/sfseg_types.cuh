@@ -42,6 +42,10 @@ struct FusedArgs {
     float taps_x[kMaxTapsXY];
     float taps_y[kMaxTapsXY];
     float taps_t[kMaxTapsT];
+    // FAST kernel (fused_rs.cuh): tap pairs (w[e], w[e-1]), w[-1] = w[2R+1] = 0,
+    // so two neighbouring outputs take one input with one FFMA2
+    float2 tpair_x[kMaxTapsXY + 1];
+    float2 tpair_y[kMaxTapsXY + 1];
     float inv_alpha;
     float one, zero;  // 1.0f / 0.0f at run time (keeps ptxas from contracting EXACT FFMA2 pairs)
     int T, H, W, pitch;

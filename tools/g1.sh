@@ -1,4 +1,2 @@
-for c in "4,8,8 1,3,3" "9,130,100 2,5,5"; do
-  timeout 60 python tools/dbg_fast.py $c 2>&1 | tail -1
-done
-timeout 120 python tools/time_solve.py --arith fast 2>&1 | tail -1
+timeout 1200 python -m pytest tests -q -m gpu -x 2>&1 | tail -4
+bash tools/profile_round.sh r01b 2>&1 | tail -15

@@ -18,7 +18,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --no-cpu-baseline > "$OUT/bench_under_ncu.log" 2>&1 || echo "launch list failed"
 for a in fast exact; do
   timeout 200 python tools/prof_run.py --iters 3 --arith $a > "$OUT/plain_$a.log" 2>&1 && \
-  timeout 400 ncu --set full --clock-control none --import-source on -k regex:fused_step_ws -s 1 -c 1 \
+  timeout 400 ncu --set full --clock-control none --import-source on -k regex:fused_step_ -s 1 -c 1 \
     -o "$OUT/full_$a" python tools/prof_run.py --iters 3 --arith $a > "$OUT/ncu_full_$a.log" 2>&1 || echo "full capture $a failed"
 done
 ls -la "$OUT"
