@@ -55,13 +55,30 @@
 #ifndef SFK_RS_LSU
 #define SFK_RS_LSU 0
 #endif
+// SFK_RS_SPX=1 (with the TMEM ring): A passes S^p and F of the output points
+// to B through the x-pass buffer (it reads them from the halo box anyway), B
+// keeps them in the TMEM ring slot of their plane: no recombination operand
+// loads at all, so the L2 -> SM traffic is the halo boxes alone
+#ifndef SFK_RS_SPX
+#define SFK_RS_SPX 0
+#endif
+// SFK_RS_STG=1: y_{k+1} leaves by plain coalesced stores instead of a TMA
+// store; SFK_RS_PRODUCER: the A thread that issues the halo-box TMA loads
+// (default thread 0; moving it to a one-block warp measured 2.7% slower)
+#ifndef SFK_RS_STG
+#define SFK_RS_STG 0
+#endif
+#ifndef SFK_RS_PRODUCER
+#define SFK_RS_PRODUCER 0
+#endif
 
 namespace sfk {
 
 // TY: tile rows; BR: output rows per B thread (a B warp covers BR rows x 32
 // columns, so there are TY / BR B warps)
-template <int RT, int R, int NWA, int STAGES, int TY_ = 64, int BR_ = 8>
+template <int RT, int R, int NWA, int STAGES, int TY_ = 64, int BR_ = 8, bool TMR_ = (SFK_RS_TMR != 0)>
 struct RsGeom {
+    static constexpr bool TMR = TMR_;  // t-pass ring in tensor memory
     static constexpr int TY = TY_, TX = 32, BR = BR_;
     static constexpr bool SPLIT = SFK_RS_SPLIT != 0;
     static constexpr int NWB = TY / BR;
@@ -96,7 +113,9 @@ struct RsGeom {
     static constexpr int TXU = TX + 4, TXQ = 2 * TX + 4;
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;
     static constexpr int XBP = (BH * TXQ + 31) / 32 * 32;
-    static constexpr int XBUF = XBU + XBP;
+    static constexpr bool SPX = SFK_RS_SPX != 0 && TMR_ && (2 * RT + 1) * 5 * BR_ <= 256;
+    static constexpr int XBS = SPX ? TY * TXU : 0;  // S^p rows of the output points (F follows)
+    static constexpr int XBUF = XBU + XBP + 2 * XBS;
     static constexpr int NBANDS = TY / 4;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NIN * FB;
 #ifndef SFK_RS_NXB
@@ -107,7 +126,8 @@ struct RsGeom {
     // per B warp: S^p and F of its BR output rows (TMA, loaded one emitted
     // plane ahead) and the staging rows of y_{k+1} for the TMA store
     static constexpr int SLAB = BR * TX;
-    static constexpr size_t SL_FLOATS = size_t(NWB) * 3 * SLAB;
+    static constexpr int SLW = SPX ? 1 : 3;  // per-warp slab rows: S^p, F, y staging (SPX: staging)
+    static constexpr size_t SL_FLOATS = size_t(NWB) * SLW * SLAB;
     static constexpr int NBAR = STAGES + 2 * SFK_RS_NXB + NWB + (SPLIT ? 2 * NWB * NS : 0);
     static constexpr size_t SMEM_BYTES = (RAW_FLOATS + XB_FLOATS + SL_FLOATS) * sizeof(float) + NBAR * 8;
     // setmaxnreg budgets. Warp w runs on SMSP w % 4, whose register file
@@ -150,10 +170,10 @@ struct RsGeom {
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
-template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool ACC>
-__global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
+template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool TMR_, bool ACC>
+__global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT, 1)
     fused_step_rs(const __grid_constant__ FusedArgs a) {
-    using G = RsGeom<RT, R, NWA, STAGES, TY_, BR_>;
+    using G = RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>;
     using A = Arith<true>;
     constexpr int BR = G::BR, TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K, NWB = G::NWB;
     constexpr int BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4, SW = G::SW;
@@ -229,7 +249,8 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
             ++prod_count;
             prodq.next();
         };
-        if (tid == 0) {
+        constexpr int PROD = SFK_RS_PRODUCER;
+        if (tid == PROD) {
             prodq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
             prod_count = 0;
             for (int s = 0; s < STAGES; ++s) issue_next();
@@ -284,6 +305,17 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
 #pragma unroll
             for (int v = 0; v < SW / 2; ++v)
                 dp[v] = make_float4(op[2 * v].x, op[2 * v].y, op[2 * v + 1].x, op[2 * v + 1].y);
+            if constexpr (G::SPX) {
+                // S^p and F of this strip's output points (box columns HX ..)
+                if (r >= R && r < R + TY) {
+                    float4* ds = reinterpret_cast<float4*>(xbp + G::XBP + (r - R) * TXU + sx * SW);
+#pragma unroll
+                    for (int v = 0; v < SW / 4; ++v) {
+                        ds[v] = py[FB / 4 + G::HX / 4 + v];
+                        ds[G::XBS / 4 + v] = py[2 * (FB / 4) + G::HX / 4 + v];
+                    }
+                }
+            }
         };
 
         PlaneStream q;
@@ -317,7 +349,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
             if (tid == 0) SFK_T(cnt, 4);
-            if (tid == 0) {
+            if (tid == PROD) {
                 fence_proxy_async();  // generic reads of stage s before the TMA overwrite
                 issue_next();
             }
@@ -538,7 +570,8 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
         // sigmoid iterations (mode 2) normalised on load, iteration 1 has none
         const float scale = st.mode == 1 ? st.inv_f : 1.0f;
 
-        constexpr bool TMR = SFK_RS_TMR != 0;
+        constexpr bool TMR = G::TMR;
+        constexpr bool LSU_MODE = SFK_RS_LSU != 0;
         constexpr int KR = TMR ? 1 : K;  // register ring depth
         float2 ringu[BR / 2][KR];  // u of rows (2k, 2k+1)
         float2 ringp[BR][KR];      // (F u, F^2 u) of row r
@@ -552,16 +585,22 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
         // TMEM ring (TMR): slot = 3 BR words (u pairs, then (F u, F^2 u) per
         // row) in this thread's TMEM lane; warps w and w + 4 share a lane
         // quadrant and take the two column halves
-        constexpr int RW = 3 * BR;
-        static_assert(!TMR || (BR == 8 && K * RW <= 128), "TMEM ring of one thread");
+        constexpr bool SPX = G::SPX;
+        static_assert(!SPX || !LSU_MODE, "SPX and LSU are alternatives");
+        constexpr int RW = (SPX ? 5 : 3) * BR;  // slot: u pairs, (F u, F^2 u) pairs [, S^p, F]
+        constexpr int TCOLS = K * RW <= 128 ? 256 : 512;  // allocation; each warp takes half
+        static_assert(!TMR || (BR == 8 && NWB == 8 && K * RW <= TCOLS / 2), "TMEM ring of one thread");
+        static_assert(TMR || K <= 7, "register ring depth");
         uint32_t tm_ring = 0;
+        int rslot = 0;  // TMR: ring slot of the current plane (runtime)
         if constexpr (TMR) {
-            if (wb == 0) tmem_alloc<256>(&tmem_base_sh);
+            if (wb == 0) tmem_alloc<TCOLS>(&tmem_base_sh);
             tcgen05_fence_before();
             named_bar_sync(2, NB);
             tcgen05_fence_after();
             const int wq = (NWA + wb) & 3;  // CTA warp id % 4
-            tm_ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) + static_cast<uint32_t>((wb >> 2) * 128);
+            tm_ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) +
+                      static_cast<uint32_t>((wb >> 2) * (TCOLS / 2));
         }
         auto ring_ld = [&](int slot, float2 (&lu)[BR / 2], float2 (&lp)[BR]) {
             float w[3][8];
@@ -579,7 +618,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
         // emitted plane ahead (cursor eq walks the output planes in schedule
         // order); zero-filled outside the volume, so those points come out as
         // exactly 0, add nothing to the sums, and the TMA store clips them
-        float* slab = bsl + wb * 3 * SLAB;
+        float* slab = bsl + wb * G::SLW * SLAB;
         uint64_t* sfull = &slab_full[wb];
         PlaneStream& eq = slabq[wb];  // lane 0 only
         auto issue_slab = [&]() {
@@ -590,8 +629,8 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
             tma_load_3d(slab + SLAB, &a.tm_fc[0], sfull, x, y, t);
             eq.next();
         };
-        constexpr bool LSU = SFK_RS_LSU != 0;
-        if (lane == 0 && !(SFK_RS_EXP & 16) && !LSU) {
+        constexpr bool LSU = LSU_MODE;
+        if (lane == 0 && !(SFK_RS_EXP & 16) && !LSU && !SPX) {
             eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
             issue_slab();
         }
@@ -634,17 +673,29 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
             constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
+            const int slot = TMR ? rslot : S_;
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const bool emit = q.p - RT >= q.ta;
             const int to = tg - RT;
 
             // y-pass (conv3d.cpp:113-135) into this plane's ring slot
+            float pso[SPX ? BR : 1], pfo[SPX ? BR : 1];  // SPX: S^p, F of this plane's points
+#pragma unroll
+            for (int r = 0; r < (SPX ? BR : 1); ++r) pso[r] = pfo[r] = 0.0f;
             if (valid) {
                 const int b = cnt % NXB;
                 if (bt == 0) SFK_T(cnt, 6);
                 mbar_wait(&xb_full[b], (cnt / NXB) & 1);
                 if (bt == 0) SFK_T(cnt, 7);
+                if constexpr (SPX) {
+                    const float* xs = xb + b * XBUF + XBU + G::XBP + (BR * wb) * TXU + lane;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        pso[r] = xs[r * TXU];
+                        pfo[r] = xs[G::XBS + r * TXU];
+                    }
+                }
                 const float* xbu = xb + b * XBUF + (BR * wb) * TXU + lane;
                 const float2* xbp = reinterpret_cast<const float2*>(xb + b * XBUF + XBU + (BR * wb) * TXQ) + lane;
                 if constexpr (TMR) {
@@ -713,7 +764,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
 #pragma unroll
                             for (int r = 0; r < BR; ++r) lp[r] = ringp[r][0];
                         } else {
-                            ring_ld((S_ + 1 + d) % K, lu, lp);
+                            ring_ld((slot + 1 + d) % K, lu, lp);
                         }
                         const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
 #pragma unroll
@@ -739,7 +790,13 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
                 }
                 if (bt == 0) SFK_T(ecnt, 9);
                 float spv[BR], fv[BR];
-                if constexpr (LSU) {
+                if constexpr (SPX) {
+                    // plane `to` sits RT slots after the oldest of the window
+                    const int sl = (slot + 1 + RT) % K;
+                    tmem_ld8(tm_ring + sl * RW + 3 * BR, spv);
+                    tmem_ld8(tm_ring + sl * RW + 4 * BR, fv);
+                    tmem_wait_ld();
+                } else if constexpr (LSU) {
 #pragma unroll
                     for (int r = 0; r < BR; ++r) {
                         spv[r] = nsp[r];
@@ -775,7 +832,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
                     for (int r = 0; r < BR; ++r)
                         if (r < nr && ox + lane < a.W) v[r] += po[static_cast<size_t>(r) * a.pitch];
                 }
-                if constexpr (LSU) {
+                if constexpr (LSU || SFK_RS_STG) {
                     const int nr = a.H - oy;
                     float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * rowstep + ox + lane;
 #pragma unroll
@@ -783,7 +840,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
                         if (r < nr) po[r * rowstep] = v[r];
                 } else {
                     // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
-                    float* ost = slab + 2 * SLAB;
+                    float* ost = slab + (G::SLW - 1) * SLAB;
                     if (lane == 0) bulk_wait_read0();  // the previous store has read the staging
                     __syncwarp();
 #pragma unroll
@@ -827,7 +884,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
                     w[2 * k] = ringu[k][0].x;
                     w[2 * k + 1] = ringu[k][0].y;
                 }
-                tmem_st8(tm_ring + S_ * RW, w);
+                tmem_st8(tm_ring + slot * RW, w);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -835,13 +892,20 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
                         w[2 * r] = ringp[4 * h + r][0].x;
                         w[2 * r + 1] = ringp[4 * h + r][0].y;
                     }
-                    tmem_st8(tm_ring + S_ * RW + 8 + 8 * h, w);
+                    tmem_st8(tm_ring + slot * RW + 8 + 8 * h, w);
                 }
+                if constexpr (SPX) {
+                    tmem_st8(tm_ring + slot * RW + 3 * BR, pso);
+                    tmem_st8(tm_ring + slot * RW + 4 * BR, pfo);
+                }
+                rslot = rslot + 1 == K ? 0 : rslot + 1;
             }
             q.next();
         };
         using std::integral_constant;
-        while (!q.done) {
+        if constexpr (TMR) {
+            while (!q.done) plane(integral_constant<int, 0>{});  // runtime slots
+        } else while (!q.done) {
             plane(integral_constant<int, 0>{});
             if constexpr (K > 1) { if (q.done) break; plane(integral_constant<int, (K > 1 ? 1 : 0)>{}); }
             if constexpr (K > 2) { if (q.done) break; plane(integral_constant<int, (K > 2 ? 2 : 0)>{}); }
@@ -856,7 +920,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_>::NT, 1)
             tcgen05_fence_before();
             named_bar_sync(2, NB);
             tcgen05_fence_after();
-            if (wb == 0) tmem_dealloc<256>(tmem_base_sh);
+            if (wb == 0) tmem_dealloc<TCOLS>(tmem_base_sh);
         }
     }
 }

@@ -247,10 +247,10 @@ FusedVariant variant_ws() {
 #define SFK_RS_BR 8
 #endif
 // FAST: products formed in registers inside the x-pass (fused_rs.cuh)
-template <int RT, int R, int NWA = SFK_RS_NWA, int ST = SFK_RS_STAGES, int TY = SFK_RS_TY,
-          int BR = SFK_RS_BR>
+template <int RT, int R, int ST = SFK_RS_STAGES, bool TMR = (SFK_RS_TMR != 0), int NWA = SFK_RS_NWA,
+          int TY = SFK_RS_TY, int BR = SFK_RS_BR>
 FusedVariant variant_rs() {
-    using G = sfk::RsGeom<RT, R, NWA, ST, TY, BR>;
+    using G = sfk::RsGeom<RT, R, NWA, ST, TY, BR, TMR>;
     FusedVariant v;
     v.rt = RT;
     v.r = R;
@@ -259,15 +259,18 @@ FusedVariant variant_rs() {
     v.fma = true;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, false>;
-    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, true>;
+    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
+    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
 }
 
-#define SFK_VARIANTS_RS() \
-    variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>()
+// radii beyond (2, 5) (BASELINE c2: 3,7,7; c4: 4,10,10): 2 TMA stages and the
+// t-pass ring in tensor memory (a 7- or 9-plane register ring does not fit)
+#define SFK_VARIANTS_RS()                                                                  \
+    variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>(),       \
+        variant_rs<3, 7, 2, true>(), variant_rs<4, 10, 2, true>()
 
 #define SFK_VARIANTS_WS(FMA_)                                                             \
     variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \

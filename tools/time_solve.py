@@ -14,8 +14,9 @@ ap.add_argument("--lib", nargs="*", default=[str(N.CUDA_LIB)])
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--arith", default="fast")
+ap.add_argument("--frames", type=int, default=None)
 a = ap.parse_args()
-prob = synth.config(a.config)[0]
+prob = synth.config(a.config, frames=a.frames)[0]
 fs, _ = prob.generate()
 cfg = prob.cfg
 cfg.arith = a.arith
@@ -37,12 +38,18 @@ for path in a.lib:
     lib.sfseg_solve(h, C.byref(q), 1, a.iters, None)
     lib.sfseg_ctx_set_timing(h, 1)
     res = []
+    import time
+    walls = []
     for _ in range(3):
+        lib.sfseg_ctx_synchronize(h)
+        t0 = time.perf_counter()
         rc = lib.sfseg_solve(h, C.byref(q), 1, a.iters, None)
+        lib.sfseg_ctx_synchronize(h)
+        walls.append((time.perf_counter() - t0) / a.iters)
         tm = N.Timing()
         lib.sfseg_ctx_get_timing(h, C.byref(tm))
         res.append(tm.step_kernel_ms / max(1, tm.step_launches))
     err = lib.sfseg_last_error().decode() if rc else ""
-    print(f"{path}: rc={rc} {err} launch_us={1e3 * min(res):.1f} (runs {[round(1e3 * r, 1) for r in res]})",
-          flush=True)
+    print(f"{path}: rc={rc} {err} launch_us={1e3 * min(res):.1f} (runs {[round(1e3 * r, 1) for r in res]}) "
+          f"wall_ms_per_iteration={1e3 * min(walls):.3f}", flush=True)
     lib.sfseg_ctx_destroy(h)
