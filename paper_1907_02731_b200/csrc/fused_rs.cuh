@@ -71,6 +71,11 @@
 #ifndef SFK_RS_PRODUCER
 #define SFK_RS_PRODUCER 0
 #endif
+// SFK_RS_DEFRED=1: the reductions of an emitted plane run at the start of
+// the next plane's y-pass, so their shuffle chains overlap its FMAs
+#ifndef SFK_RS_DEFRED
+#define SFK_RS_DEFRED 0
+#endif
 
 namespace sfk {
 
@@ -670,6 +675,36 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
         int cnt = 0;   // in-volume planes consumed
         int ecnt = 0;  // output planes emitted
 
+        // canonical reduction (device_common.cuh) of one emitted plane: BR / 4
+        // blocks of 4 rows per warp, one column per lane, fp32 within a block
+        constexpr bool DEFRED = SFK_RS_DEFRED != 0;
+        float dv[BR];
+        int d_to = 0, d_tx = 0, d_ty = 0;
+        bool dpend = false;
+        auto reduce_plane = [&](const float (&v)[BR], int to, int tx, int ty) {
+#pragma unroll
+            for (int h = 0; h < BR / 4; ++h) {
+                float cs = 0.0f;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+                const int gb = ty * G::NBANDS + (BR / 4) * wb + h;
+                if (lane == 0 && gb < a.nbands && tx < a.nhalves)
+                    a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + tx] =
+                        static_cast<double>(cs);
+            }
+            float cmax = 0.0f;
+#pragma unroll
+            for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
+            const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+            if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
+        };
+        auto flush_red = [&]() {
+            if (dpend) reduce_plane(dv, d_to, d_tx, d_ty);
+            dpend = false;
+        };
+
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
             constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
@@ -688,6 +723,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                 if (bt == 0) SFK_T(cnt, 6);
                 mbar_wait(&xb_full[b], (cnt / NXB) & 1);
                 if (bt == 0) SFK_T(cnt, 7);
+                if constexpr (DEFRED) flush_red();
                 if constexpr (SPX) {
                     const float* xs = xb + b * XBUF + XBU + G::XBP + (BR * wb) * TXU + lane;
 #pragma unroll
@@ -855,25 +891,17 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                 if (bt == 0) SFK_T(ecnt, 11);
                 ++ecnt;
                 if (last) {
-                    // canonical reduction (device_common.cuh): BR / 4 blocks of
-                    // 4 rows per warp, one column per lane, fp32 within a block
+                    if constexpr (DEFRED) {
+                        flush_red();
 #pragma unroll
-                    for (int h = 0; h < BR / 4; ++h) {
-                        float cs = 0.0f;
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
-#pragma unroll
-                        for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-                        const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + h;
-                        if (lane == 0 && gb < a.nbands && q.tile_x < a.nhalves)
-                            a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
-                                static_cast<double>(cs);
+                        for (int r = 0; r < BR; ++r) dv[r] = v[r];
+                        d_to = to;
+                        d_tx = q.tile_x;
+                        d_ty = q.tile_y;
+                        dpend = true;
+                    } else {
+                        reduce_plane(v, to, q.tile_x, q.tile_y);
                     }
-                    float cmax = 0.0f;
-#pragma unroll
-                    for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
-                    const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
-                    if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
                 }
             }
             if constexpr (TMR) {
@@ -914,6 +942,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             if constexpr (K > 5) { if (q.done) break; plane(integral_constant<int, (K > 5 ? 5 : 0)>{}); }
             if constexpr (K > 6) { if (q.done) break; plane(integral_constant<int, (K > 6 ? 6 : 0)>{}); }
         }
+        flush_red();
         if (lane == 0) bulk_wait0();  // the output rows are written before the CTA exits
         if constexpr (TMR) {
             tmem_wait_st();
