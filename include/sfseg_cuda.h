@@ -154,6 +154,24 @@ int sfseg_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
 int sfseg_solve(sfseg_ctx* ctx, const sfseg_params* p, int32_t first_iter,
                 int32_t last_iter, sfseg_iter_record* records);
 
+/* Convergence criteria of sfseg_solve_until. */
+enum sfseg_conv {
+    SFSEG_CONV_STEP = 0,  /* ||x_k - x_{k-1}||_2 < tol        (oracle.cpp:234-242, power_iteration) */
+    SFSEG_CONV_ANGLE = 1  /* angle(x_k, x_{k-1}) < tol degrees (bench.cpp:75-80, converged_conv) */
+};
+
+/* sfseg_solve with an early exit (the reference's run() has none; its
+ * power_iteration and bench converged_conv stop on the criteria above).
+ * Runs iterations first_iter..max_iter and stops after the first iteration
+ * whose projected iterate x_k meets the criterion against x_{k-1} (for the
+ * first iteration of a solve, x_0 is S or x0 as stored, like converged_conv's
+ * start from features.unary). *iterations_done receives the last iteration
+ * run; records (may be NULL) then holds *iterations_done-first_iter+1
+ * entries. One 32-byte read-back per iteration. */
+int sfseg_solve_until(sfseg_ctx* ctx, const sfseg_params* p, int32_t first_iter,
+                      int32_t max_iter, int32_t criterion, double tol,
+                      int32_t* iterations_done, sfseg_iter_record* records);
+
 /* Copies the current iterate (the projected unit vector after the last solved
  * iteration) to soft (may be NULL) and threshold_final(soft, frac) to mask
  * (may be NULL). */

@@ -28,6 +28,7 @@ SFSEG_ARITH_EXACT = 0
 SFSEG_ARITH_FAST = 1
 SFSEG_MEM_HOST = 0
 SFSEG_MEM_DEVICE = 1
+SFSEG_CONV_STEP, SFSEG_CONV_ANGLE = 0, 1  # enum sfseg_conv
 
 
 class Error(RuntimeError):
@@ -143,6 +144,8 @@ _SIGS = {
     "sfseg_ctx_stream": (C.c_void_p, [_P]),
     "sfseg_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, _I32]),
     "sfseg_solve": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, C.POINTER(IterRecord)]),
+    "sfseg_solve_until": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, _I32, C.c_double,
+                                    C.POINTER(C.c_int32), C.POINTER(IterRecord)]),
     "sfseg_download": (C.c_int, [_P, C.c_double, _P, _P, _I32]),
     "sfseg_metrics": (C.c_int, [_P, _P, _P, C.c_double, C.POINTER(C.c_double),
                                 C.POINTER(C.c_double), _I32]),

@@ -298,6 +298,58 @@ __global__ void k_metrics(Vol xv, Vol ref, const uint8_t* gt, const float* maxp,
     }
 }
 
+// Convergence statistics between two consecutive projected iterates
+// x_k = T_k(y_k) and x_{k-1} = T_{k-1}(y_{k-1}) (materialised as k_transform
+// does; prev_raw: x_{k-1} is the start vector S / x0 as stored):
+// per-block fp64 sums of x_k x_{k-1}, x_k^2, x_{k-1}^2 and (x_k - x_{k-1})^2,
+// written to part[block][4]; k_conv_final sums the blocks in block order,
+// so the result does not depend on timing.
+__device__ __forceinline__ float project_state(float a, const IterState& st) {
+    float r = a;
+    if (st.mode >= 1) r = static_cast<float>(static_cast<double>(a) * st.inv);
+    if (st.mode == 2) {
+        const double z = st.lambda * (static_cast<double>(r) - st.theta);
+        r = static_cast<float>(1.0 / (1.0 + exp(-z)));
+    }
+    return r;
+}
+
+__global__ void k_conv_stats(Vol cur, const IterState* st_cur, Vol prev, const IterState* st_prev,
+                             int prev_raw, double* part) {
+    __shared__ double s[4][kAuxThreads];
+    const IterState sc = *st_cur;
+    const IterState sp = *st_prev;
+    double d = 0.0, na = 0.0, nb = 0.0, df = 0.0;
+    SFK_FOR_VOXELS(cur, t, y, x) {
+        const double a = project_state(cur.p[cur.at(t, y, x)], sc);
+        const float pb = prev.p[prev.at(t, y, x)];
+        const double b = prev_raw ? pb : project_state(pb, sp);
+        d += a * b;
+        na += a * a;
+        nb += b * b;
+        df += (a - b) * (a - b);
+    }
+    s[0][threadIdx.x] = d;
+    s[1][threadIdx.x] = na;
+    s[2][threadIdx.x] = nb;
+    s[3][threadIdx.x] = df;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k)
+            for (int j = 0; j < 4; ++j) s[j][threadIdx.x] += s[j][threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_conv_final(const double* part, int nblocks, double* out4) {
+    if (threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int b = 0; b < nblocks; ++b) acc += part[b * 4 + threadIdx.x];
+        out4[threadIdx.x] = acc;
+    }
+}
+
 // ---- generic (any-radius) stencil: conv3d.cpp:80-167 on pitched volumes --
 
 struct Taps {

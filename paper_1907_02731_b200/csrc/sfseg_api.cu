@@ -388,6 +388,8 @@ struct sfseg_ctx {
     float* bminmax = nullptr;
     double* acc3 = nullptr;
     unsigned long long* cnt2 = nullptr;
+    double* conv_part = nullptr;     // convergence statistics (solve_until)
+    IterState* st_prev = nullptr;
     // persistent-grid schedule (device copy, keyed by ntiles/Tout/G)
     int4* sched_seg = nullptr;
     int* sched_off = nullptr;
@@ -872,6 +874,58 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
         if (norms[i] == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
 }
 
+// Fixed-count solve with an early exit: the reference's
+// run() always runs cfg.iterations; power_iteration stops once
+// ||x_k - x_{k-1}||_2 < tol (oracle.cpp:234-242) and bench.cpp's
+// converged_conv once angle(x_k, x_{k-1}) < tol degrees (bench.cpp:75-80,
+// metrics.cpp:22-38). Each iteration here is the same fused step + finalize
+// as solve_impl, then k_conv_stats against the previous projected iterate and
+// one 32-byte read-back for the host's test.
+void solve_until_impl(sfseg_ctx* c, const sfseg_params* p, int first, int max_iter, int criterion,
+                      double tol, int32_t* done, sfseg_iter_record* rec) {
+    if (criterion != SFSEG_CONV_STEP && criterion != SFSEG_CONV_ANGLE)
+        fail(SFSEG_ERR_PARAMETER, "unknown convergence criterion");
+    if (!(tol >= 0.0)) fail(SFSEG_ERR_PARAMETER, "tolerance must be >= 0");
+    validate_params(p);
+    if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_solve_until before sfseg_load");
+    if (first < 1 || max_iter < first) fail(SFSEG_ERR_PARAMETER, "bad iteration range");
+    if (first > 1 && c->cur < 0) fail(SFSEG_ERR_STATE, "continuing a solve that never started");
+    const int nb = aux_grid(c);
+    if (!c->conv_part) {
+        ck(cudaMalloc(&c->conv_part, (static_cast<size_t>(nb) * 4 + 4) * sizeof(double)), "malloc");
+        ck(cudaMalloc(&c->st_prev, sizeof(IterState)), "malloc");
+    }
+    int it = first;
+    for (; it <= max_iter; ++it) {
+        // x_{k-1}: the visible iterate before this step
+        const bool prev_raw = c->cur < 0;
+        const float* prev = prev_raw ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
+        ck(cudaMemcpyAsync(c->st_prev, c->st, sizeof(IterState), cudaMemcpyDeviceToDevice, c->stream),
+           "state copy");
+        sfseg_iter_record r{};
+        solve_impl(c, p, it, it, rec ? &r : nullptr);  // syncs; throws on a zero norm
+        if (rec) rec[it - first] = r;
+        sfk::k_conv_stats<<<nb, sfk::kAuxThreads, 0, c->stream>>>(
+            c->vol(c->y[c->cur]), c->st, c->vol(const_cast<float*>(prev)), c->st_prev, prev_raw,
+            c->conv_part);
+        sfk::k_conv_final<<<1, 32, 0, c->stream>>>(c->conv_part, nb, c->conv_part + 4 * nb);
+        launched(c->stream, "k_conv_stats");
+        double h[4];
+        ck(cudaMemcpyAsync(h, c->conv_part + 4 * nb, sizeof h, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        bool stop;
+        if (criterion == SFSEG_CONV_STEP) {
+            stop = std::sqrt(h[3]) < tol;
+        } else {
+            if (h[1] == 0.0 || h[2] == 0.0) fail(SFSEG_ERR_PARAMETER, "angle is undefined for a zero vector");
+            const double cs = std::clamp(h[0] / (std::sqrt(h[1]) * std::sqrt(h[2])), -1.0, 1.0);
+            stop = std::acos(cs) * 57.295779513082320876798154814105 < tol;
+        }
+        if (stop) break;
+    }
+    *done = std::min(it, max_iter);
+}
+
 void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
                const float* const* F, const float* x0, int32_t mem) {
     check_shape(T, H, W);
@@ -1041,6 +1095,8 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         cudaFree(c->bminmax);
         cudaFree(c->acc3);
         cudaFree(c->cnt2);
+        if (c->conv_part) cudaFree(c->conv_part);
+        if (c->st_prev) cudaFree(c->st_prev);
         if (c->norms) cudaFree(c->norms);
         if (c->sched_seg) cudaFree(c->sched_seg);
         if (c->sched_off) cudaFree(c->sched_off);
@@ -1110,6 +1166,17 @@ int sfseg_solve(sfseg_ctx* c, const sfseg_params* p, int32_t first, int32_t last
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         solve_impl(c, p, first, last, rec);
+    });
+}
+
+int sfseg_solve_until(sfseg_ctx* c, const sfseg_params* p, int32_t first, int32_t max_iter,
+                      int32_t criterion, double tol, int32_t* iterations_done,
+                      sfseg_iter_record* records) {
+    return guarded([&] {
+        if (!c || !p || !iterations_done) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        solve_until_impl(c, p, first, max_iter, criterion, tol, iterations_done, records);
     });
 }
 

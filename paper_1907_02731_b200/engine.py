@@ -485,3 +485,52 @@ def run(features: FeatureSet, cfg: SfsegConfig, x0=None, reference=None, ground_
         ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
         N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold), ob.ptr, mb.ptr, mem))
     return RunResult(soft, mask, trace)
+
+
+def run_until_converged(features: FeatureSet, cfg: SfsegConfig, tol: float,
+                        criterion: str = "angle", max_iterations: Optional[int] = None,
+                        x0=None, ctx: Optional[Context] = None):
+    """Power iteration with an early exit (sfseg_solve_until).
+
+    The reference's run() always performs cfg.iterations; its power_iteration
+    stops once ||x_k - x_{k-1}||_2 < tol (oracle.cpp:234-242, criterion
+    "step") and bench.cpp's converged_conv once angle(x_k, x_{k-1}) < tol
+    degrees (bench.cpp:75-80, criterion "angle"). Returns (RunResult,
+    iterations_done); the result's trace has one record per iteration run.
+    """
+    crit = {"step": N.SFSEG_CONV_STEP, "angle": N.SFSEG_CONV_ANGLE}.get(criterion)
+    if crit is None:
+        raise ParameterError("criterion must be 'step' or 'angle'")
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    max_it = int(max_iterations if max_iterations is not None else cfg.iterations)
+    sb = _Buf(features.unary)
+    shape = _shape3(sb.shape)
+    if len(features.pairwise) == 0:
+        raise ValidationError("feature set needs at least one pairwise channel")
+    fbs = [_Buf(f, shape) for f in features.pairwise]
+    bufs = [sb] + fbs
+    x0b = _Buf(x0, shape) if x0 is not None else None
+    if x0b is not None:
+        bufs.append(x0b)
+    mem = _same_mem(bufs)
+    T, H, W = shape
+    lib = ctx._lib
+    soft = _empty_like(sb)
+    mask = _empty_like(sb, np.uint8)
+    trace = RunTrace()
+    recs = (N.IterRecord * max_it)()
+    done = C.c_int32()
+    with ctx.lock:
+        N.check(lib.sfseg_load(ctx.handle, T, H, W, len(fbs), sb.ptr,
+                               C.cast(_channel_ptrs(fbs), C.c_void_p),
+                               x0b.ptr if x0b else None, mem))
+        N.check(lib.sfseg_solve_until(ctx.handle, C.byref(p), 1, max_it, crit, float(tol),
+                                      C.byref(done), recs))
+        for r in recs[:done.value]:
+            trace.iterations.append(IterationRecord(r.iter, r.l2_norm_pre_normalize,
+                                                    wall_time_s=r.wall_time_s))
+        ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
+        N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold), ob.ptr, mb.ptr, mem))
+    return RunResult(soft, mask, trace), done.value

@@ -123,3 +123,13 @@ def test_synth_rng_is_the_reference_stream():
     ref = Reference()
     assert np.array_equal(synth.xoshiro_u64(42, 100), ref.xoshiro_u64(42, 100))
     assert np.array_equal(synth.xoshiro_gaussian(42, 100), ref.xoshiro_gaussian(42, 100))
+
+
+def test_convergence_criterion_is_validated_on_the_host():
+    """run_until_converged rejects an unknown stopping rule before any device
+    work (the C ABI returns SFSEG_ERR_PARAMETER for it as well)."""
+    from paper_1907_02731_b200 import engine as E
+
+    fs = E.FeatureSet(np.zeros((2, 4, 4), np.float32), [np.zeros((2, 4, 4), np.float32)])
+    with pytest.raises(E.ParameterError):
+        E.run_until_converged(fs, E.SfsegConfig(), 1e-6, criterion="residual")
