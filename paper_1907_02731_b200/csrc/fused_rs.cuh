@@ -76,8 +76,38 @@
 #ifndef SFK_RS_DEFRED
 #define SFK_RS_DEFRED 0
 #endif
+// SFK_RS_WIDE=1: one CTA-wide TMA load of the S^p / F tile per emitted plane
+// and one TMA store of the y tile (two B-wide barriers per plane) instead of a
+// load pair and a store per B warp: 3 TMA operations per plane instead of 24
+#ifndef SFK_RS_WIDE
+#define SFK_RS_WIDE 1
+#endif
+// SFK_RS_RAWFENCE=0: no proxy fence before the producer refills a box stage
+// (the stage's generic reads have completed: their values were consumed before
+// the named barrier that precedes the refill)
+// SFK_RS_WREDUCE=1 (WIDE): one B warp per plane finishes the column-sum
+// butterflies from shared memory instead of every warp shuffling (238 us vs
+// 214 us: the reducing warp delays the next barrier)
+#ifndef SFK_RS_WREDUCE
+#define SFK_RS_WREDUCE 0
+#endif
+#ifndef SFK_RS_RAWFENCE
+#define SFK_RS_RAWFENCE 1
+#endif
 
 namespace sfk {
+
+// the 32-column xor-butterfly (16, 8, 4, 2, 1) of device_common.cuh evaluated
+// serially on 32 column sums, in fp32: the same operands in the same order,
+// so the same bits as the shuffle butterfly
+__device__ __forceinline__ float tree32f_s4(const float* v, int i) {
+    const float a = (v[i] + v[i + 16]) + (v[i + 8] + v[i + 24]);
+    const float b = (v[i + 4] + v[i + 20]) + (v[i + 12] + v[i + 28]);
+    return a + b;
+}
+__device__ __forceinline__ float tree32f(const float* v) {
+    return (tree32f_s4(v, 0) + tree32f_s4(v, 2)) + (tree32f_s4(v, 1) + tree32f_s4(v, 3));
+}
 
 // TY: tile rows; BR: output rows per B thread (a B warp covers BR rows x 32
 // columns, so there are TY / BR B warps)
@@ -202,6 +232,10 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
     __shared__ PlaneStream slabq[NWB];
     __shared__ int prod_count;
     __shared__ uint32_t tmem_base_sh;
+    // WIDE: per-plane column sums of y^2 per 4-row band and per-warp maxima,
+    // reduced by one B warp after the store barrier
+    __shared__ float red_cols[SFK_RS_WIDE && SFK_RS_WREDUCE ? TY_ / 4 : 1][32];
+    __shared__ float red_max[SFK_RS_WIDE && SFK_RS_WREDUCE ? TY_ / BR_ : 1];
 
     const int tid = threadIdx.x;
     if (a.st->degenerate && SFK_RS_EXP == 0) return;  // an earlier iteration hit a zero norm
@@ -355,7 +389,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             named_bar_sync(1, NA);     // raw stage s fully read
             if (tid == 0) SFK_T(cnt, 4);
             if (tid == PROD) {
-                fence_proxy_async();  // generic reads of stage s before the TMA overwrite
+                if (SFK_RS_RAWFENCE) fence_proxy_async();  // generic reads of stage s before the TMA overwrite
                 issue_next();
             }
             ++cnt;
@@ -623,19 +657,27 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
         // emitted plane ahead (cursor eq walks the output planes in schedule
         // order); zero-filled outside the volume, so those points come out as
         // exactly 0, add nothing to the sums, and the TMA store clips them
-        float* slab = bsl + wb * G::SLW * SLAB;
-        uint64_t* sfull = &slab_full[wb];
-        PlaneStream& eq = slabq[wb];  // lane 0 only
+        constexpr bool WIDE = SFK_RS_WIDE != 0 && !TMR;
+        constexpr bool WRED = WIDE && SFK_RS_WREDUCE != 0;
+        static_assert(!WIDE || G::SLW == 3, "WIDE: S^p, F and y tiles");
+        // WIDE: [S^p tile][F tile][y tile] of TY x TX; this warp's rows at BR wb
+        float* slab = WIDE ? bsl + (BR * wb) * TX : bsl + wb * G::SLW * SLAB;
+        constexpr int SLSTEP = WIDE ? TY * TX : SLAB;  // distance S^p -> F -> y rows
+        uint64_t* sfull = WIDE ? &slab_full[0] : &slab_full[wb];
+        PlaneStream& eq = slabq[WIDE ? 0 : wb];  // lane 0 (WIDE: thread bt == 0) only
         auto issue_slab = [&]() {
             if (eq.done) return;
-            mbar_arrive_expect_tx(sfull, 2 * SLAB * sizeof(float));
-            const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
-            tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
-            tma_load_3d(slab + SLAB, &a.tm_fc[0], sfull, x, y, t);
+            constexpr int NSL = WIDE ? TY * TX : SLAB;
+            mbar_arrive_expect_tx(sfull, 2 * NSL * sizeof(float));
+            const int x = eq.tile_x * TX, y = eq.tile_y * TY + (WIDE ? 0 : BR * wb),
+                      t = a.out_t0 + eq.p - a.buf_t0;
+            float* dst = WIDE ? bsl : slab;
+            tma_load_3d(dst, &a.tm_spc, sfull, x, y, t);
+            tma_load_3d(dst + NSL, &a.tm_fc[0], sfull, x, y, t);
             eq.next();
         };
         constexpr bool LSU = LSU_MODE;
-        if (lane == 0 && !(SFK_RS_EXP & 16) && !LSU && !SPX) {
+        if ((WIDE ? bt == 0 : lane == 0) && !(SFK_RS_EXP & 16) && !LSU && !SPX) {
             eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
             issue_slab();
         }
@@ -839,6 +881,19 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                         fv[r] = nf[r];
                     }
                     fetch();  // the next emitted plane's operands
+                } else if constexpr (WIDE) {
+                    mbar_wait(sfull, ecnt & 1);
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        spv[r] = slab[r * TX + lane];
+                        fv[r] = slab[SLSTEP + r * TX + lane];
+                    }
+                    if (bt == 0) bulk_wait_read0();  // the previous y tile store has read the staging
+                    named_bar_sync(3, NB);            // every B warp has read the slab
+                    if (bt == 0) {
+                        fence_proxy_async();
+                        issue_slab();
+                    }
                 } else {
                     if (!(SFK_RS_EXP & 16)) mbar_wait(sfull, ecnt & 1);
 #pragma unroll
@@ -874,6 +929,46 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
 #pragma unroll
                     for (int r = 0; r < BR; ++r)
                         if (r < nr) po[r * rowstep] = v[r];
+                } else if constexpr (WIDE) {
+                    float* ost = slab + 2 * SLSTEP;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) ost[r * TX + lane] = v[r];
+                    fence_proxy_async();
+                    if (last && WRED) {
+                        // column sums of this warp's 4-row bands and its max; the
+                        // butterfly runs in one warp after the barrier
+#pragma unroll
+                        for (int h = 0; h < BR / 4; ++h) {
+                            float cs = 0.0f;
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
+                            red_cols[(BR / 4) * wb + h][lane] = cs;
+                        }
+                        float cmax = 0.0f;
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
+                        const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                        if (lane == 0) red_max[wb] = __int_as_float(wm);
+                    }
+                    named_bar_sync(3, NB);
+                    if (bt == 0) {
+                        tma_store_3d(&a.tm_out, bsl + 2 * SLSTEP, ox, q.tile_y * TY, to - a.out_buf_t0);
+                        bulk_commit();
+                    }
+                    if (last && WRED && wb == (ecnt % NWB)) {  // the reducing warp rotates per plane
+                        if (lane < G::NBANDS) {
+                            const int gb = q.tile_y * G::NBANDS + lane;
+                            const float sb = tree32f(red_cols[lane]);
+                            if (gb < a.nbands && q.tile_x < a.nhalves)
+                                a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
+                                    static_cast<double>(sb);
+                        } else if (lane == 31) {
+                            float m = 0.0f;
+#pragma unroll
+                            for (int w = 0; w < NWB; ++w) m = fmaxf(m, red_max[w]);
+                            atomic_max_nonneg(a.frame_max + (to - a.part_t0), m);
+                        }
+                    }
                 } else {
                     // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
                     float* ost = slab + (G::SLW - 1) * SLAB;
@@ -890,7 +985,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                 }
                 if (bt == 0) SFK_T(ecnt, 11);
                 ++ecnt;
-                if (last) {
+                if (last && !WRED) {
                     if constexpr (DEFRED) {
                         flush_red();
 #pragma unroll

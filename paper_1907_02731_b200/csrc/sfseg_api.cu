@@ -189,6 +189,7 @@ struct FusedVariant {
     void (*kernel)(FusedArgs);
     void (*kernel_acc)(FusedArgs);  // later channel groups (y += terms); may equal kernel
     int box_w, box_h;
+    int slab_h = 8;  // rows of the recombination-operand / output TMA boxes
 };
 
 template <int RT, int R, int TY, int TX, bool FMA>
@@ -259,6 +260,7 @@ FusedVariant variant_rs() {
     v.fma = true;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
+    v.slab_h = (SFK_RS_WIDE && !TMR) ? TY : 8;
     v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
     v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, true>;
     v.box_w = G::BW;
@@ -666,8 +668,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         std::memset(&a, 0, sizeof a);
         a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
         a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
-        a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, 8);
-        a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->tx, 8);
+        a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, v->slab_h);
+        a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->tx, v->slab_h);
         a.sp = c->sp;
         a.out = out;
         a.part = c->part;
@@ -706,7 +708,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         }
         for (size_t g = 0; g < Fch.size(); ++g) {
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
-            a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->tx, 8);
+            a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->tx, v->slab_h);
             a.f[0] = Fch[g];
             a.first_group = g == 0;
             a.last_group = g + 1 == Fch.size();
