@@ -102,6 +102,16 @@ __global__ void k_unit_range(Vol v, const float* lohi) {
     }
 }
 
+// Q = sum_c f_c^2 in channel order (fused_mc.cuh, FAST): one launch per
+// channel, q = f*f for the first, then q = fma(f, f, q)
+__global__ void k_sq_acc(Vol q, Vol f, int first) {
+    SFK_FOR_VOXELS(q, t, y, x) {
+        const size_t i = q.at(t, y, x);
+        const float v = f.p[i];
+        q.p[i] = first ? v * v : fmaf(v, v, q.p[i]);
+    }
+}
+
 // pow_volume (engine.cpp:52-71): float(pow(double s, p)); p==0 -> 1, p==1 -> copy
 __global__ void k_pow(Vol s, Vol out, double p) {
     SFK_FOR_VOXELS(s, t, y, x) {
@@ -167,16 +177,19 @@ __global__ void k_finalize_frames(const double* part, int per_frame, double* fra
 // Total over frames (fixed order: same tree as above over frame index) and
 // the scalars the next iteration applies on load (engine.cpp:168-205).
 // mode_next: 1 = normalise, 2 = normalise + sigmoid; lambda from the host.
-__global__ void k_finalize_total(const double* frame_sum, float* frame_max, int T,
-                                 IterState* st, double* norms, int iter_index, int mode_next,
-                                 double lambda, double threshold_frac) {
+// Shared by k_finalize_total and the last block of k_finalize (one block of
+// kAuxThreads threads); frame_sum is read through L2 (written by other blocks).
+__device__ __forceinline__ void finalize_total_block(const double* frame_sum, float* frame_max, int T,
+                                                     IterState* st, double* norms, int iter_index,
+                                                     int mode_next, double lambda,
+                                                     double threshold_frac) {
     __shared__ double s[kAuxThreads];
     __shared__ float sm[kAuxThreads];
     double acc = 0.0;
     float m = 0.0f;
     for (int i = threadIdx.x; i < T; i += blockDim.x) {
-        acc += frame_sum[i];
-        m = fmaxf(m, frame_max[i]);
+        acc += __ldcg(frame_sum + i);
+        m = fmaxf(m, __ldcg(frame_max + i));
         frame_max[i] = 0.0f;  // reset for the next iteration
     }
     s[threadIdx.x] = acc;
@@ -210,6 +223,46 @@ __global__ void k_finalize_total(const double* frame_sum, float* frame_max, int 
         }
         *st = n;
     }
+}
+
+__global__ void k_finalize_total(const double* frame_sum, float* frame_max, int T,
+                                 IterState* st, double* norms, int iter_index, int mode_next,
+                                 double lambda, double threshold_frac) {
+    finalize_total_block(frame_sum, frame_max, T, st, norms, iter_index, mode_next, lambda,
+                         threshold_frac);
+}
+
+// k_finalize_frames + k_finalize_total in one launch (one per iteration
+// instead of two): block t sums frame t exactly as k_finalize_frames, and the
+// last block to finish runs finalize_total_block (threadfence-reduction
+// pattern; *ticket is 0 on entry and is reset by that block). Same operands in
+// the same order as the two-launch path, so the same bits.
+__global__ void k_finalize(const double* part, int per_frame, double* frame_sum, float* frame_max,
+                           unsigned int* ticket, IterState* st, double* norms, int iter_index,
+                           int mode_next, double lambda, double threshold_frac) {
+    __shared__ double s[kAuxThreads];
+    __shared__ bool is_last;
+    const int t = blockIdx.x;
+    const double* p = part + static_cast<size_t>(t) * per_frame;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < per_frame; i += blockDim.x) acc += p[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        frame_sum[t] = s[0];
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    finalize_total_block(frame_sum, frame_max, gridDim.x, st, norms, iter_index, mode_next, lambda,
+                         threshold_frac);
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // x = T(y): the projection of the state, materialised into a volume.

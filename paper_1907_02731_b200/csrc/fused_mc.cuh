@@ -1,0 +1,457 @@
+// fused_mc.cuh — SFSeg power-iteration step for several feature channels,
+// FAST arithmetic, in the (C + 2)-field form.
+//
+// Summing the per-channel recombination (engine.cpp:107-120) over the
+// channels (engine.cpp:157-162) and using the linearity of the separable
+// convolution G (conv3d.cpp:171-185) gives
+//
+//   sum_c X_c = S^p [ (C/alpha - Q) G(u) - G(Q u) + 2 sum_c f_c G(f_c u) ],
+//   u = S^p x,  Q = sum_c f_c^2  (static: computed once per solve),
+//
+// so a step needs C + 2 convolved fields instead of the 1 + 2C of the
+// per-channel form (c2, C = 8: 10 fields instead of 24; c4, C = 3: 5 instead
+// of 9). All of them in one pass would need a t-pass ring of
+// (2 RT + 1) x (C + 2) planes per output tile (c2: 573 KB for a 64 x 32 tile),
+// which no on-chip memory holds, so the fields run in groups of NF <= 2 per
+// launch, each a single pass over the volume:
+//
+//   HEAD (first launch): raw boxes x, S^p, Q; fields u and Q u;
+//        y  = S^p ((C/alpha - Q) G(u) - G(Q u)); also writes u to U
+//   TAIL (later launches): raw boxes U, f_a [, f_b]; fields f_a u [, f_b u];
+//        y += 2 S^p (f_a G(f_a u) + f_b G(f_b u))
+//
+// The schedule, roles and pipeline are those of fused_step_rs (fused_rs.cuh)
+// with its t-pass ring in tensor memory: one 512-thread CTA per SM walking
+// (64 x 32 tile, frame range) segments; 8 A warps issue the halo-box TMA loads
+// and run the x-pass with the products formed in registers; 8 B warps run the
+// y-pass into a TMEM ring of the last 2RT+1 planes, the t-pass, the
+// recombination (x 1/||y_k||, deferred as in FAST), the TMA store and, in the
+// last launch, the canonical reductions. Every field is one "single" slot:
+// two neighbouring outputs take one input with one FFMA2 and a tap pair
+// (w[e], w[e-1]) — columns in the x-pass, rows in the y-pass.
+#pragma once
+
+#include "device_common.cuh"
+#include "fused_step.cuh"  // PlaneStream, Arith, ffma2
+#include "sfseg_types.cuh"
+
+namespace sfk {
+
+template <int RT, int R, int NF, bool HEAD>
+struct McGeom {
+    static constexpr int TY = 64, TX = 32, BR = 8, NWA = 8, NWB = TY / BR, STAGES = 2;
+    static constexpr int NA = 32 * NWA, NB = 32 * NWB, NT = NA + NB;
+    static constexpr int K = 2 * RT + 1;
+    static constexpr int BH = TY + 2 * R;
+    static constexpr int HX = (R + 3) / 4 * 4;  // left halo (16-byte aligned box start)
+    static constexpr int HR = ((TX + HX + HX) / 4) % 2 == 1 ? HX : HX + 4;  // odd float4 rows
+    static constexpr int BW = TX + HX + HR, BW4 = BW / 4;
+    static constexpr int XOFF = HX - R;
+    static constexpr int FB = (BH * BW + 31) / 32 * 32;
+    static constexpr int NR = NF + 1;  // raw boxes: HEAD x, S^p, Q; TAIL U, f_a [, f_b]
+    static constexpr int SW = 8;
+    static constexpr int NINX = SW + 2 * R;
+    static constexpr int NLD = (XOFF + NINX + 3) / 4;
+    static constexpr int RBLK = (BH + 7) / 8;
+    static constexpr int XPASS = (RBLK + NWA - 1) / NWA;
+    static constexpr int TXU = TX + 4;
+    static constexpr int XBU = (BH * TXU + 31) / 32 * 32;  // one field of the x-pass output
+    static constexpr int NXB = 2;
+    static constexpr int NOP = HEAD ? 2 : NF + 1;  // recombination operands: S^p, Q | S^p, f_a [, f_b]
+    static constexpr int SLAB = BR * TX;
+    static constexpr size_t RAW_FLOATS = size_t(STAGES) * NR * FB;
+    static constexpr size_t XB_FLOATS = size_t(NXB) * NF * XBU;
+    static constexpr size_t SL_FLOATS = size_t(NWB) * (NOP + 1) * SLAB;  // + y staging
+    static constexpr int NBAR = STAGES + 2 * NXB + NWB;
+    static constexpr size_t SMEM_BYTES = (RAW_FLOATS + XB_FLOATS + SL_FLOATS) * sizeof(float) + NBAR * 8;
+    static constexpr int NBANDS = TY / 4;
+    // TMEM ring: slot = NF x BR words (row pairs of each field) per thread;
+    // warps w and w + 4 share a lane quadrant and take half the columns each
+    static constexpr int RW = NF * BR;
+    static constexpr int TCOLS = K * RW <= 128 ? 256 : 512;
+    static constexpr int RA = 64;
+    static constexpr int RB = 192;  // 2 A + 2 B warps per SMSP: (512 - 2 * 64) / 2
+    static_assert(BW4 % 2 == 1, "odd float4 box rows (conflict-free strip reads)");
+    static_assert((TXU / 4) % 2 == 1, "conflict-free x-pass rows");
+    static_assert(BW <= 256 && BH <= 256, "TMA box limit");
+    static_assert(K * RW <= TCOLS / 2, "TMEM ring of one thread");
+    static_assert(NF >= 1 && NF <= 2 && (NF == 2 || !HEAD), "field groups");
+    static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
+};
+
+template <int RT, int R, int NF, bool HEAD>
+__global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
+    fused_step_mc(const __grid_constant__ FusedArgs a) {
+    using G = McGeom<RT, R, NF, HEAD>;
+    using A = Arith<true>;
+    constexpr int BR = G::BR, TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K, NWB = G::NWB;
+    constexpr int BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4, SW = G::SW, NR = G::NR;
+    constexpr int TXU = G::TXU, XBU = G::XBU, SLAB = G::SLAB, NXB = G::NXB, STAGES = G::STAGES;
+    constexpr int NOP = G::NOP, RW = G::RW;
+
+    extern __shared__ __align__(128) float smem[];
+    float* raw = smem;                // [STAGES][NR][FB]
+    float* xb = raw + G::RAW_FLOATS;  // [NXB][NF][XBU]
+    float* bsl = xb + G::XB_FLOATS;   // [NWB][NOP + 1][BR][TX]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(bsl + G::SL_FLOATS);
+    uint64_t* raw_full = mbar;                      // [STAGES]
+    uint64_t* xb_full = mbar + STAGES;              // [NXB] (count NA)
+    uint64_t* xb_empty = mbar + STAGES + NXB;       // [NXB] (count NB)
+    uint64_t* slab_full = mbar + STAGES + 2 * NXB;  // [NWB]
+
+    __shared__ IterState st;
+    __shared__ PlaneStream prodq;
+    __shared__ PlaneStream slabq[NWB];
+    __shared__ int prod_count;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int tid = threadIdx.x;
+    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
+    if (s0 >= s1) return;
+
+    if (tid == 0) {
+        st = *a.st;
+        for (int s = 0; s < STAGES; ++s) mbar_init(&raw_full[s], 1);
+        for (int b = 0; b < NXB; ++b) {
+            mbar_init(&xb_full[b], NA);
+            mbar_init(&xb_empty[b], NB);
+        }
+        for (int w = 0; w < NWB; ++w) mbar_init(&slab_full[w], 1);
+        fence_barrier_init();
+        prefetch_tensormap(&a.tm_x);
+        if (HEAD) prefetch_tensormap(&a.tm_sp);
+        prefetch_tensormap(&a.tm_f[0]);
+        prefetch_tensormap(&a.tm_out);
+        prefetch_tensormap(&a.tm_spc);
+        prefetch_tensormap(&a.tm_fc[0]);
+    }
+    __syncthreads();
+    const float2 zero2 = make_float2(0.0f, 0.0f);
+
+    if (tid < NA) {
+        // =====================================================================
+        // A: TMA producer + x-pass (conv3d.cpp:88-101) with in-register products
+        // =====================================================================
+        setmaxnreg_dec<G::RA>();
+        auto issue_next = [&]() {
+            while (!prodq.done) {
+                const int tg = a.out_t0 + prodq.p;
+                if (tg >= 0 && tg < a.T) break;
+                prodq.next();
+            }
+            if (prodq.done) return;
+            const int tg = a.out_t0 + prodq.p;
+            const int s = prod_count % STAGES;
+            float* dst = raw + static_cast<size_t>(s) * NR * FB;
+            uint64_t* bar = &raw_full[s];
+            mbar_arrive_expect_tx(bar, NR * BH * BW * sizeof(float));
+            const int bx = prodq.tile_x * TX - G::HX, by = prodq.tile_y * TY - R, bt = tg - a.buf_t0;
+            tma_load_3d(dst, &a.tm_x, bar, bx, by, bt);
+            if constexpr (HEAD) {
+                tma_load_3d(dst + FB, &a.tm_sp, bar, bx, by, bt);
+                tma_load_3d(dst + 2 * FB, &a.tm_f[0], bar, bx, by, bt);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NF; ++i) tma_load_3d(dst + (1 + i) * FB, &a.tm_f[i], bar, bx, by, bt);
+            }
+            ++prod_count;
+            prodq.next();
+        };
+        if (tid == 0) {
+            prodq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            prod_count = 0;
+            for (int s = 0; s < STAGES; ++s) issue_next();
+        }
+        const bool sigm = HEAD && st.mode == 2;
+        const int xw = tid >> 5, xl = tid & 31;  // lane -> (row xl & 7, strip xl >> 3)
+
+        // one x-pass item: box row r, strip sx (SW outputs as column pairs)
+        auto item = [&](auto sig_c, const float* rs, float* xbb, int r, int sx, float* urow) {
+            constexpr bool SIG = decltype(sig_c)::value;
+            const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + 2 * sx;
+            float2 ou[NF][SW / 2];
+            float uc[SW];  // HEAD: u at this strip's own points (for U)
+            float4 v[NR];
+#pragma unroll
+            for (int m4 = 0; m4 < G::NLD * 4; ++m4) {
+                if (m4 % 4 == 0) {
+#pragma unroll
+                    for (int i = 0; i < NR; ++i) v[i] = py[i * (FB / 4) + m4 / 4];
+                }
+                const int m = m4 - G::XOFF;
+                if (m < 0 || m >= G::NINX) continue;
+                const int c = m4 % 4;
+                float e4[NR];
+#pragma unroll
+                for (int i = 0; i < NR; ++i) e4[i] = c == 0 ? v[i].x : c == 1 ? v[i].y : c == 2 ? v[i].z : v[i].w;
+                float phi[NF];
+                if constexpr (HEAD) {
+                    const float x = SIG ? A::load_sigmoid(e4[0], st) : e4[0];
+                    const float u = e4[1] * x;  // engine.cpp:92-100
+                    phi[0] = u;
+                    phi[1] = e4[2] * u;  // Q u
+                    if (m >= R && m < R + SW) uc[m - R] = u;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NF; ++i) phi[i] = e4[1 + i] * e4[0];  // f_i u
+                }
+#pragma unroll
+                for (int i = 0; i < NF; ++i) {
+#pragma unroll
+                    for (int k = 0; k < SW / 2; ++k) {
+                        const int e = m - 2 * k;
+                        if (e < 0 || e > 2 * R + 1) continue;
+                        ou[i][k] = ffma2(make_float2(phi[i], phi[i]), a.tpair_x[e], e == 0 ? zero2 : ou[i][k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NF; ++i) {
+                float4* du = reinterpret_cast<float4*>(xbb + i * XBU + r * TXU + sx * SW);
+#pragma unroll
+                for (int w = 0; w < SW / 4; ++w)
+                    du[w] = make_float4(ou[i][2 * w].x, ou[i][2 * w].y, ou[i][2 * w + 1].x, ou[i][2 * w + 1].y);
+            }
+            if constexpr (HEAD) {
+                if (urow) {
+                    float4* pu = reinterpret_cast<float4*>(urow + sx * SW);
+                    pu[0] = make_float4(uc[0], uc[1], uc[2], uc[3]);
+                    pu[1] = make_float4(uc[4], uc[5], uc[6], uc[7]);
+                }
+            }
+        };
+
+        PlaneStream q;
+        q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+        int cnt = 0;
+        for (; !q.done; q.next()) {
+            const int tg = a.out_t0 + q.p;
+            if (tg < 0 || tg >= a.T) continue;  // planes outside the volume: B zero-fills
+            const int s = cnt % STAGES;
+            const int b = cnt % NXB;
+            mbar_wait(&raw_full[s], (cnt / STAGES) & 1);
+            mbar_wait(&xb_empty[b], ((cnt / NXB) & 1) ^ 1);
+            const float* rs = raw + static_cast<size_t>(s) * NR * FB;
+            float* xbb = xb + static_cast<size_t>(b) * NF * XBU;
+#pragma unroll
+            for (int k = 0; k < G::XPASS; ++k) {
+                const int blk = xw + k * G::NWA;
+                if (blk >= G::RBLK) break;
+                const int r = blk * 8 + (xl & 7);
+                if (r >= BH) continue;
+                float* urow = nullptr;  // HEAD: U row of this item's output points
+                if constexpr (HEAD) {
+                    const int oy = q.tile_y * TY + r - R;
+                    if (r >= R && r < R + TY && oy < a.H)
+                        urow = a.u_out + (static_cast<size_t>(tg - a.buf_t0) * a.H + oy) * a.pitch +
+                               q.tile_x * TX;
+                }
+                if (sigm)
+                    item(std::true_type{}, rs, xbb, r, xl >> 3, urow);
+                else
+                    item(std::false_type{}, rs, xbb, r, xl >> 3, urow);
+            }
+            mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
+            named_bar_sync(1, NA);     // raw stage s fully read
+            if (tid == 0) {
+                fence_proxy_async();  // generic reads of stage s before the TMA overwrite
+                issue_next();
+            }
+            ++cnt;
+        }
+    } else {
+        // =====================================================================
+        // B: y-pass into the TMEM ring, t-pass, recombination, store, reductions
+        // =====================================================================
+        setmaxnreg_inc<G::RB>();
+        const int bt = tid - NA;
+        const int lane = bt & 31;
+        const int wb = bt >> 5;
+        const bool last = a.last_group;
+        const float scale = st.mode == 1 ? st.inv_f : 1.0f;  // deferred 1/||y_k|| (FAST)
+        constexpr int TCOLS = G::TCOLS;
+        if (wb == 0) tmem_alloc<TCOLS>(&tmem_base_sh);
+        tcgen05_fence_before();
+        named_bar_sync(2, NB);
+        tcgen05_fence_after();
+        const int wq = (G::NWA + wb) & 3;  // CTA warp id % 4
+        const uint32_t tm_ring = tmem_base_sh + (static_cast<uint32_t>(32 * wq) << 16) +
+                                 static_cast<uint32_t>((wb >> 2) * (TCOLS / 2));
+
+        float* slab = bsl + static_cast<size_t>(wb) * (NOP + 1) * SLAB;
+        uint64_t* sfull = &slab_full[wb];
+        PlaneStream& eq = slabq[wb];  // lane 0 only
+        auto issue_slab = [&]() {
+            if (eq.done) return;
+            mbar_arrive_expect_tx(sfull, NOP * SLAB * sizeof(float));
+            const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
+            tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
+#pragma unroll
+            for (int i = 0; i + 1 < NOP; ++i) tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
+            eq.next();
+        };
+        if (lane == 0) {
+            eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+            issue_slab();
+        }
+
+        PlaneStream q;
+        q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+        int cnt = 0, ecnt = 0, rslot = 0;
+        while (!q.done) {
+            const int tg = a.out_t0 + q.p;
+            const bool valid = tg >= 0 && tg < a.T;
+            const bool emit = q.p - RT >= q.ta;
+            const int to = tg - RT;
+            float2 cur[NF][BR / 2];  // y-pass output of this plane, row pairs
+            if (valid) {
+                // y-pass (conv3d.cpp:113-135): rows BR wb .. + BR - 1 of column `lane`
+                const int b = cnt % NXB;
+                mbar_wait(&xb_full[b], (cnt / NXB) & 1);
+#pragma unroll
+                for (int i = 0; i < NF; ++i) {
+                    const float* xc = xb + (static_cast<size_t>(b) * NF + i) * XBU + (BR * wb) * TXU + lane;
+                    float vin[BR + 2 * R];
+#pragma unroll
+                    for (int j = 0; j < BR + 2 * R; ++j) vin[j] = xc[j * TXU];
+#pragma unroll
+                    for (int e = 0; e <= 2 * R + 1; ++e) {
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k)
+                            cur[i][k] = ffma2(make_float2(vin[2 * k + e], vin[2 * k + e]), a.tpair_y[e],
+                                              e == 0 ? zero2 : cur[i][k]);
+                    }
+                }
+                mbar_arrive(&xb_empty[b]);
+                ++cnt;
+            } else {
+#pragma unroll
+                for (int i = 0; i < NF; ++i)
+#pragma unroll
+                    for (int k = 0; k < BR / 2; ++k) cur[i][k] = zero2;
+            }
+            if (emit) {
+                // t-pass (conv3d.cpp:147-165): K - 1 ring slots (oldest first), then this plane
+                float2 tacc[NF][BR / 2];
+                tmem_wait_st();
+#pragma unroll
+                for (int d = 0; d < K; ++d) {
+                    float2 lu[NF][BR / 2];
+                    if (d == K - 1) {
+#pragma unroll
+                        for (int i = 0; i < NF; ++i)
+#pragma unroll
+                            for (int k = 0; k < BR / 2; ++k) lu[i][k] = cur[i][k];
+                    } else {
+                        int sl = rslot + 1 + d;
+                        sl = sl >= K ? sl - K : sl;
+                        float w[NF][8];
+#pragma unroll
+                        for (int i = 0; i < NF; ++i) tmem_ld8(tm_ring + sl * RW + 8 * i, w[i]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < NF; ++i)
+#pragma unroll
+                            for (int k = 0; k < BR / 2; ++k) lu[i][k] = make_float2(w[i][2 * k], w[i][2 * k + 1]);
+                    }
+                    const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
+#pragma unroll
+                    for (int i = 0; i < NF; ++i)
+#pragma unroll
+                        for (int k = 0; k < BR / 2; ++k) tacc[i][k] = ffma2(lu[i][k], w2, d == 0 ? zero2 : tacc[i][k]);
+                }
+                mbar_wait(sfull, ecnt & 1);
+                float opv[NOP][BR];
+#pragma unroll
+                for (int o = 0; o < NOP; ++o)
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) opv[o][r] = slab[o * SLAB + r * TX + lane];
+                __syncwarp();
+                if (lane == 0) {
+                    fence_proxy_async();  // the reads above before the next TMA write
+                    issue_slab();
+                }
+                const int ox = q.tile_x * TX, oy = q.tile_y * TY + BR * wb;
+                float v[BR];
+#pragma unroll
+                for (int r = 0; r < BR; ++r) {
+                    float g[NF];
+#pragma unroll
+                    for (int i = 0; i < NF; ++i) g[i] = (r & 1) ? tacc[i][r / 2].y : tacc[i][r / 2].x;
+                    if constexpr (HEAD) {
+                        // S^p ((C/alpha - Q) G(u) - G(Q u))
+                        v[r] = (opv[0][r] * scale) * ((a.c_inv_alpha - opv[1][r]) * g[0] - g[1]);
+                    } else {
+                        // 2 S^p sum_i f_i G(f_i u)
+                        float sfg = opv[1][r] * g[0];
+                        if constexpr (NF > 1) sfg = fmaf(opv[2][r], g[1], sfg);
+                        v[r] = (2.0f * opv[0][r] * scale) * sfg;
+                    }
+                }
+                if constexpr (!HEAD) {  // y of the earlier launches; rows past H read nothing
+                    const int nr = a.H - oy;
+                    const float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * a.pitch + ox + lane;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r)
+                        if (r < nr && ox + lane < a.W) v[r] += po[static_cast<size_t>(r) * a.pitch];
+                }
+                // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
+                float* ost = slab + NOP * SLAB;
+                if (lane == 0) bulk_wait_read0();  // the previous store has read the staging
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < BR; ++r) ost[r * TX + lane] = v[r];
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&a.tm_out, ost, ox, oy, to - a.out_buf_t0);
+                    bulk_commit();
+                }
+                ++ecnt;
+                if (last) {
+                    // canonical reduction (device_common.cuh): 4-row blocks, fp32
+                    // column sums, xor-butterfly over the 32 columns
+#pragma unroll
+                    for (int h = 0; h < BR / 4; ++h) {
+                        float cs = 0.0f;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+                        const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + h;
+                        if (lane == 0 && gb < a.nbands && q.tile_x < a.nhalves)
+                            a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
+                                static_cast<double>(cs);
+                    }
+                    float cmax = 0.0f;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
+                    const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                    if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
+                }
+            }
+            // this plane into ring slot rslot (it held a plane no longer needed)
+#pragma unroll
+            for (int i = 0; i < NF; ++i) {
+                float w[8];
+#pragma unroll
+                for (int k = 0; k < BR / 2; ++k) {
+                    w[2 * k] = cur[i][k].x;
+                    w[2 * k + 1] = cur[i][k].y;
+                }
+                tmem_st8(tm_ring + rslot * RW + 8 * i, w);
+            }
+            rslot = rslot + 1 == K ? 0 : rslot + 1;
+            q.next();
+        }
+        if (lane == 0) bulk_wait0();  // the output rows are written before the CTA exits
+        tmem_wait_st();
+        tcgen05_fence_before();
+        named_bar_sync(2, NB);
+        tcgen05_fence_after();
+        if (wb == 0) tmem_dealloc<TCOLS>(tmem_base_sh);
+    }
+}
+
+}  // namespace sfk

@@ -24,6 +24,7 @@
 #include "fused_step.cuh"
 #include "fused_ws.cuh"
 #include "fused_rs.cuh"
+#include "fused_mc.cuh"
 
 namespace {
 
@@ -274,6 +275,40 @@ FusedVariant variant_rs() {
     variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>(),       \
         variant_rs<3, 7, 2, true>(), variant_rs<4, 10, 2, true>()
 
+// FAST, C > 1: (C + 2)-field launches (fused_mc.cuh): a HEAD (u, Q u) and
+// TAILs of one or two channels (f_a u [, f_b u])
+struct McVariant {
+    int rt, r;
+    int threads, box_w, box_h;
+    size_t smem[3];          // head, tail of 2 channels, tail of 1
+    void (*kernel[3])(FusedArgs);
+};
+
+template <int RT, int R>
+McVariant variant_mc() {
+    McVariant v;
+    v.rt = RT;
+    v.r = R;
+    using GH = sfk::McGeom<RT, R, 2, true>;
+    using G2 = sfk::McGeom<RT, R, 2, false>;
+    using G1 = sfk::McGeom<RT, R, 1, false>;
+    v.threads = GH::NT;
+    v.box_w = GH::BW;
+    v.box_h = GH::BH;
+    v.smem[0] = GH::SMEM_BYTES;
+    v.smem[1] = G2::SMEM_BYTES;
+    v.smem[2] = G1::SMEM_BYTES;
+    v.kernel[0] = sfk::fused_step_mc<RT, R, 2, true>;
+    v.kernel[1] = sfk::fused_step_mc<RT, R, 2, false>;
+    v.kernel[2] = sfk::fused_step_mc<RT, R, 1, false>;
+    return v;
+}
+
+const std::vector<McVariant>& mc_variants() {
+    static const std::vector<McVariant> v = {variant_mc<2, 5>(), variant_mc<3, 7>(), variant_mc<4, 10>()};
+    return v;
+}
+
 #define SFK_VARIANTS_WS(FMA_)                                                             \
     variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \
         variant_ws<2, 5, FMA_>()
@@ -350,6 +385,22 @@ const FusedVariant* pick_variant(int rt, int ry, int rx, bool fma) {
     return best;
 }
 
+// SFSEG_MC=0 keeps the per-channel launches for FAST multi-channel steps
+const McVariant* pick_mc(int rt, int ry, int rx) {
+    static const bool off = [] {
+        const char* e = std::getenv("SFSEG_MC");
+        return e && *e == '0';
+    }();
+    if (off || env_flag("SFSEG_FORCE_GENERIC")) return nullptr;
+    const int r = std::max(ry, rx);
+    const McVariant* best = nullptr;
+    for (const auto& v : mc_variants())
+        if (v.rt >= rt && v.r >= r &&
+            (!best || (2L * v.rt + 1) * (2L * v.r + 1) < (2L * best->rt + 1) * (2L * best->r + 1)))
+            best = &v;
+    return best;
+}
+
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 }  // namespace
@@ -381,6 +432,7 @@ struct sfseg_ctx {
     size_t part_elems = 0;
     double* frame_sum = nullptr;
     float* frame_max = nullptr;
+    unsigned int* ticket = nullptr;  // k_finalize's last-block counter (0 between launches)
     IterState* st = nullptr;     // solve state
     IterState* st_aux = nullptr; // stateless operators
     double* norms = nullptr;
@@ -398,6 +450,8 @@ struct sfseg_ctx {
     long long sched_key = -1;
     // generic-path temporaries (allocated lazily)
     std::vector<float*> tmp;
+    float* q = nullptr;              // Q = sum_c f_c^2 of the channel set q_for (fused_mc.cuh)
+    std::vector<float*> q_for;
     // dense staging for host transfers (one contiguous DMA, re-pitched on the
     // device) and the device mask of downloads
     float* stage = nullptr;
@@ -450,6 +504,8 @@ void release_problem(sfseg_ctx* c) {
     dfree(c->y[1]);
     for (auto*& t : c->tmp) dfree(t);
     c->tmp.clear();
+    dfree(c->q);
+    c->q_for.clear();
     if (c->stage) cudaFree(c->stage);
     if (c->dmask) cudaFree(c->dmask);
     c->stage = nullptr;
@@ -655,6 +711,108 @@ float* tmp_vol(sfseg_ctx* c, size_t i) {
     return c->tmp[i];
 }
 
+// Q = sum_c f_c^2 for the channel set Fch (cached until the channels change)
+float* ensure_q(sfseg_ctx* c, const std::vector<float*>& Fch) {
+    if (c->q && c->q_for == Fch) return c->q;
+    if (!c->q) c->q = dalloc_vol(c);
+    for (size_t i = 0; i < Fch.size(); ++i)
+        sfk::k_sq_acc<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->q), c->vol(Fch[i]),
+                                                                      i == 0);
+    launched(c->stream, "k_sq_acc");
+    c->q_for = Fch;
+    return c->q;
+}
+
+// FAST step for C > 1 channels in the (C + 2)-field form (fused_mc.cuh): a
+// HEAD launch (u, Q u; writes u) and ceil(C / 2) TAIL launches of one or two
+// channels accumulating into y; the last launch emits the reductions
+void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
+                    const IterState* st, float* out, const std::vector<float*>& Fch,
+                    const McVariant& v) {
+    float* q = ensure_q(c, Fch);
+    float* u = tmp_vol(c, 0);
+    FusedVariant fv;  // taps / tensor-map geometry
+    fv.rt = v.rt;
+    fv.r = v.r;
+    fv.ty = 64;
+    fv.tx = 32;
+    FusedArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+    a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, fv.tx, 8);
+    a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, fv.tx, 8);
+    a.sp = c->sp;
+    a.out = out;
+    a.u_out = u;
+    a.part = c->part;
+    a.frame_max = c->frame_max;
+    a.part_t0 = c->out_t0;
+    a.st = st;
+    fill_taps(a, k, fv);
+    a.inv_alpha = static_cast<float>(1.0 / alpha);
+    a.c_inv_alpha = static_cast<float>(static_cast<double>(Fch.size()) / alpha);
+    a.one = 1.0f;
+    a.zero = 0.0f;
+    a.T = c->Tg;
+    a.H = c->H;
+    a.W = c->W;
+    a.pitch = c->P;
+    a.buf_t0 = c->buf_t0;
+    a.out_t0 = c->out_t0;
+    a.out_t1 = c->out_t1;
+    a.out_buf_t0 = c->buf_t0;
+    a.tiles_x = (c->W + fv.tx - 1) / fv.tx;
+    a.tiles_y = (c->H + fv.ty - 1) / fv.ty;
+    a.nbands = c->nbands();
+    a.nhalves = c->nhalves();
+    const int grid_n = c->num_sms;
+    upload_schedule(c, a.tiles_x * a.tiles_y, c->Tout(), grid_n);
+    a.sched = c->sched_seg;
+    a.sched_off = c->sched_off;
+    static bool attr_set[16] = {};
+    const int vidx = static_cast<int>(&v - mc_variants().data());
+    if (!attr_set[vidx]) {
+        for (int i = 0; i < 3; ++i)
+            ck(cudaFuncSetAttribute(v.kernel[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(v.smem[i])),
+               "cudaFuncSetAttribute");
+        attr_set[vidx] = true;
+    }
+    const int C = static_cast<int>(Fch.size());
+    const int ntail = (C + 1) / 2;
+    for (int g = 0; g <= ntail; ++g) {
+        int kind = 0;
+        if (g == 0) {
+            a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            a.tm_f[0] = make_tmap(q, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            a.tm_fc[0] = make_tmap(q, c->T, c->H, c->W, c->P, fv.tx, 8);
+        } else {
+            const int c0 = 2 * (g - 1), n = std::min(2, C - c0);
+            kind = n == 2 ? 1 : 2;
+            if (g == 1) a.tm_x = make_tmap(u, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            for (int i = 0; i < n; ++i) {
+                a.tm_f[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+                a.tm_fc[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, fv.tx, 8);
+            }
+        }
+        a.first_group = g == 0;
+        a.last_group = g == ntail;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->timing) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, c->stream);
+        }
+        v.kernel[kind]<<<grid_n, v.threads, v.smem[kind], c->stream>>>(a);
+        launched(c->stream, "fused_step_mc launch");
+        if (c->timing) {
+            cudaEventRecord(e1, c->stream);
+            c->ev.push_back(e0);
+            c->ev.push_back(e1);
+        }
+    }
+}
+
 // One step y_out = sum_c step_c(T(x_src)) with fused kernels or the generic
 // multi-pass path; emits canonical partials + frame max into c->part /
 // c->frame_max for the whole volume.
@@ -663,6 +821,11 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
     const float inv_alpha = static_cast<float>(1.0 / alpha);
     const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx, fma);
     g_conv_count.fetch_add(3ull * Fch.size(), std::memory_order_relaxed);
+    const McVariant* mc = (fma && Fch.size() > 1) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
+    if (mc) {
+        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc);
+        return;
+    }
     if (v) {
         FusedArgs a;
         std::memset(&a, 0, sizeof a);
@@ -773,10 +936,10 @@ void frame_sums(sfseg_ctx* c) {
 
 void finalize(sfseg_ctx* c, IterState* st, double* norms, int iter_index, int mode_next,
               double lambda, double frac) {
-    frame_sums(c);
-    sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
-        c->frame_sum, c->frame_max, c->Tout(), st, norms, iter_index, mode_next, lambda, frac);
-    launched(c->stream, "finalize");
+    sfk::k_finalize<<<c->Tout(), sfk::kAuxThreads, 0, c->stream>>>(
+        c->part, c->nbands() * c->nhalves(), c->frame_sum, c->frame_max, c->ticket, st, norms,
+        iter_index, mode_next, lambda, frac);
+    launched(c->stream, "k_finalize");
 }
 
 void set_state(sfseg_ctx* c, IterState* dst, const IterState& s) {
@@ -955,6 +1118,7 @@ void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
         validate_vol(c, c->x0, true, "x0");
     }
     c->resident = true;
+    c->q_for.clear();  // channel contents changed
 }
 
 // stateless helpers: (re)use the resident buffers of a scratch problem
@@ -1080,6 +1244,8 @@ int sfseg_ctx_create(int device, sfseg_ctx** out) {
         ck(cudaMalloc(&c->bminmax, 2 * aux_grid(c) * sizeof(float)), "malloc");
         ck(cudaMalloc(&c->acc3, 3 * sizeof(double)), "malloc");
         ck(cudaMalloc(&c->cnt2, 2 * sizeof(unsigned long long)), "malloc");
+        ck(cudaMalloc(&c->ticket, sizeof(unsigned int)), "malloc");
+        ck(cudaMemset(c->ticket, 0, sizeof(unsigned int)), "memset");
         *out = c;
     });
 }
@@ -1097,6 +1263,7 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         cudaFree(c->bminmax);
         cudaFree(c->acc3);
         cudaFree(c->cnt2);
+        cudaFree(c->ticket);
         if (c->conv_part) cudaFree(c->conv_part);
         if (c->st_prev) cudaFree(c->st_prev);
         if (c->norms) cudaFree(c->norms);
@@ -1489,6 +1656,7 @@ int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C
             validate_vol(c, c->x0, true, "x0");
         }
         c->resident = true;
+        c->q_for.clear();  // channel contents changed
     });
 }
 

@@ -47,6 +47,8 @@ struct FusedArgs {
     float2 tpair_x[kMaxTapsXY + 1];
     float2 tpair_y[kMaxTapsXY + 1];
     float inv_alpha;
+    float c_inv_alpha;  // C / alpha (fused_mc.cuh HEAD launch)
+    float* u_out;       // u = S^p x at the output points (fused_mc.cuh HEAD launch writes it)
     float one, zero;  // 1.0f / 0.0f at run time (keeps ptxas from contracting EXACT FFMA2 pairs)
     int T, H, W, pitch;
     int buf_t0;      // global frame of input buffer frame 0

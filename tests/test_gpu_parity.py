@@ -160,6 +160,29 @@ def test_step_fast_within_tolerance(shape, alpha, p, radii, sigmas):
     assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
 
 
+# FAST with C > 1 runs the (C + 2)-field kernels (fused_mc.cuh): a HEAD launch
+# (u, Q u) and TAIL launches of one or two channels. Same operator, regrouped,
+# so the step matches the reference within the FAST tolerance.
+MC_CASES = [
+    ((9, 70, 130), (2, 5, 5), (0.5, 1.5, 1.5), 2),
+    ((7, 45, 97), (2, 4, 4), (0.5, 1.5, 1.5), 3),
+    ((8, 96, 160), (3, 7, 7), (1e30, 5.0, 5.0), 8),
+    ((10, 90, 150), (4, 10, 10), (0.5, 1.5, 1.5), 3),
+    ((6, 67, 70), (4, 10, 10), (0.5, 1.5, 1.5), 5),
+]
+
+
+@pytest.mark.parametrize("shape,radii,sigmas,C", MC_CASES)
+def test_step_multichannel_fast_within_tolerance(shape, radii, sigmas, C):
+    S, F = _features(shape, 21, channels=C)
+    x = random_volume(shape, 77)
+    cfg = _cfg(radii, sigmas, 1.0, 0.1, arith="fast")
+    fs = E.FeatureSet(S, F)
+    got = E.sfseg_step(x, fs, cfg).astype(np.float64)
+    want = Oracle().step(x, S, F, cfg).astype(np.float64)
+    assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
+
+
 def test_run_c1_cropped_fast_matches_reference():
     prob, fs, _ = _problem(1, frames=12)
     cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": "fast"})
