@@ -35,11 +35,31 @@
 #include "fused_step.cuh"  // PlaneStream, Arith, ffma2
 #include "sfseg_types.cuh"
 
+// ablation bits (development builds, tools/ablate.sh): 1 A x-pass arithmetic
+// off, 2 B y-pass off, 4 t-pass ring loads off, 8 recombination/store off
+#ifndef SFK_MC_EXP
+#define SFK_MC_EXP 0
+#endif
+// SFK_MC_TB: t-pass ring slots loaded per tcgen05.wait::ld batch
+#ifndef SFK_MC_TB
+#define SFK_MC_TB 1
+#endif
+// x-pass (A) warps, TMA box stages, x-pass buffers
+#ifndef SFK_MC_NWA
+#define SFK_MC_NWA 8
+#endif
+#ifndef SFK_MC_STAGES
+#define SFK_MC_STAGES 2
+#endif
+#ifndef SFK_MC_NXB
+#define SFK_MC_NXB 2
+#endif
+
 namespace sfk {
 
 template <int RT, int R, int NF, bool HEAD>
 struct McGeom {
-    static constexpr int TY = 64, TX = 32, BR = 8, NWA = 8, NWB = TY / BR, STAGES = 2;
+    static constexpr int TY = 64, TX = 32, BR = 8, NWA = SFK_MC_NWA, NWB = TY / BR, STAGES = SFK_MC_STAGES;
     static constexpr int NA = 32 * NWA, NB = 32 * NWB, NT = NA + NB;
     static constexpr int K = 2 * RT + 1;
     static constexpr int BH = TY + 2 * R;
@@ -56,8 +76,10 @@ struct McGeom {
     static constexpr int XPASS = (RBLK + NWA - 1) / NWA;
     static constexpr int TXU = TX + 4;
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;  // one field of the x-pass output
-    static constexpr int NXB = 2;
-    static constexpr int NOP = HEAD ? 2 : NF + 1;  // recombination operands: S^p, Q | S^p, f_a [, f_b]
+    static constexpr int NXB = SFK_MC_NXB;
+    // recombination operands (TMA slabs, one emitted plane ahead): S^p, Q |
+    // S^p, f_a [, f_b], y of the earlier launches
+    static constexpr int NOP = HEAD ? 2 : NF + 2;
     static constexpr int SLAB = BR * TX;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NR * FB;
     static constexpr size_t XB_FLOATS = size_t(NXB) * NF * XBU;
@@ -70,13 +92,19 @@ struct McGeom {
     static constexpr int RW = NF * BR;
     static constexpr int TCOLS = K * RW <= 128 ? 256 : 512;
     static constexpr int RA = 64;
-    static constexpr int RB = 192;  // 2 A + 2 B warps per SMSP: (512 - 2 * 64) / 2
+    // setmaxnreg: every warp starts with the launch grant RPOOL (65536 / NT,
+    // multiple of 8); an SMSP holds NWA / 4 A and NWB / 4 B warps, and B can
+    // take only what A gives back (asking for more blocks forever)
+    static constexpr int RPOOL = (65536 / NT) / 8 * 8 > 255 ? 248 : (65536 / NT) / 8 * 8;
+    static constexpr int RB_ = ((NWA / 4 + NWB / 4) * RPOOL - (NWA / 4) * RA) / (NWB / 4) / 8 * 8;
+    static constexpr int RB = RB_ > 248 ? 248 : RB_;
     static_assert(BW4 % 2 == 1, "odd float4 box rows (conflict-free strip reads)");
     static_assert((TXU / 4) % 2 == 1, "conflict-free x-pass rows");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
     static_assert(K * RW <= TCOLS / 2, "TMEM ring of one thread");
     static_assert(NF >= 1 && NF <= 2 && (NF == 2 || !HEAD), "field groups");
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
+    static_assert(NWA % 4 == 0 && NWB % 4 == 0, "setmaxnreg acts on whole warpgroups");
 };
 
 template <int RT, int R, int NF, bool HEAD>
@@ -106,7 +134,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
-    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    if (a.st->degenerate && SFK_MC_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;
 
@@ -239,7 +267,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                 const int blk = xw + k * G::NWA;
                 if (blk >= G::RBLK) break;
                 const int r = blk * 8 + (xl & 7);
-                if (r >= BH) continue;
+                if (r >= BH || (SFK_MC_EXP & 1)) continue;
                 float* urow = nullptr;  // HEAD: U row of this item's output points
                 if constexpr (HEAD) {
                     const int oy = q.tile_y * TY + r - R;
@@ -288,7 +316,9 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
             const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
             tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
 #pragma unroll
-            for (int i = 0; i + 1 < NOP; ++i) tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
+            for (int i = 0; i < (HEAD ? 1 : NF); ++i) tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
+            if constexpr (!HEAD)  // y so far: written by the previous launch (stream order)
+                tma_load_3d(slab + (NOP - 1) * SLAB, &a.tm_out, sfull, x, y, t - a.buf_t0 + a.out_buf_t0);
             eq.next();
         };
         if (lane == 0) {
@@ -310,7 +340,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                 const int b = cnt % NXB;
                 mbar_wait(&xb_full[b], (cnt / NXB) & 1);
 #pragma unroll
-                for (int i = 0; i < NF; ++i) {
+                for (int i = 0; i < ((SFK_MC_EXP & 2) ? 0 : NF); ++i) {
                     const float* xc = xb + (static_cast<size_t>(b) * NF + i) * XBU + (BR * wb) * TXU + lane;
                     float vin[BR + 2 * R];
 #pragma unroll
@@ -323,6 +353,9 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                                               e == 0 ? zero2 : cur[i][k]);
                     }
                 }
+                if (SFK_MC_EXP & 2)
+                    for (int i = 0; i < NF; ++i)
+                        for (int k = 0; k < BR / 2; ++k) cur[i][k] = make_float2(xb[lane], xb[lane + 32]);
                 mbar_arrive(&xb_empty[b]);
                 ++cnt;
             } else {
@@ -335,31 +368,35 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                 // t-pass (conv3d.cpp:147-165): K - 1 ring slots (oldest first), then this plane
                 float2 tacc[NF][BR / 2];
                 tmem_wait_st();
+                constexpr int TB = SFK_MC_TB;
 #pragma unroll
-                for (int d = 0; d < K; ++d) {
-                    float2 lu[NF][BR / 2];
-                    if (d == K - 1) {
+                for (int d0 = 0; d0 < K; d0 += TB) {
+                    float w[TB][NF][8];
 #pragma unroll
-                        for (int i = 0; i < NF; ++i)
-#pragma unroll
-                            for (int k = 0; k < BR / 2; ++k) lu[i][k] = cur[i][k];
-                    } else {
+                    for (int j = 0; j < TB; ++j) {
+                        const int d = d0 + j;
+                        if (d >= K - 1 || (SFK_MC_EXP & 4)) continue;
                         int sl = rslot + 1 + d;
                         sl = sl >= K ? sl - K : sl;
-                        float w[NF][8];
 #pragma unroll
-                        for (int i = 0; i < NF; ++i) tmem_ld8(tm_ring + sl * RW + 8 * i, w[i]);
-                        tmem_wait_ld();
+                        for (int i = 0; i < NF; ++i) tmem_ld8(tm_ring + sl * RW + 8 * i, w[j][i]);
+                    }
+                    if (d0 < K - 1 && !(SFK_MC_EXP & 4)) tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < TB; ++j) {
+                        const int d = d0 + j;
+                        if (d >= K) continue;
+                        const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
 #pragma unroll
                         for (int i = 0; i < NF; ++i)
 #pragma unroll
-                            for (int k = 0; k < BR / 2; ++k) lu[i][k] = make_float2(w[i][2 * k], w[i][2 * k + 1]);
+                            for (int k = 0; k < BR / 2; ++k) {
+                                const float2 lu = (d == K - 1 || (SFK_MC_EXP & 4))
+                                                      ? cur[i][k]
+                                                      : make_float2(w[j][i][2 * k], w[j][i][2 * k + 1]);
+                                tacc[i][k] = ffma2(lu, w2, d == 0 ? zero2 : tacc[i][k]);
+                            }
                     }
-                    const float2 w2 = make_float2(a.taps_t[d], a.taps_t[d]);
-#pragma unroll
-                    for (int i = 0; i < NF; ++i)
-#pragma unroll
-                        for (int k = 0; k < BR / 2; ++k) tacc[i][k] = ffma2(lu[i][k], w2, d == 0 ? zero2 : tacc[i][k]);
                 }
                 mbar_wait(sfull, ecnt & 1);
                 float opv[NOP][BR];
@@ -376,6 +413,10 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                 float v[BR];
 #pragma unroll
                 for (int r = 0; r < BR; ++r) {
+                    if (SFK_MC_EXP & 8) {
+                        v[r] = tacc[0][r / 2].x;
+                        continue;
+                    }
                     float g[NF];
 #pragma unroll
                     for (int i = 0; i < NF; ++i) g[i] = (r & 1) ? tacc[i][r / 2].y : tacc[i][r / 2].x;
@@ -389,12 +430,9 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                         v[r] = (2.0f * opv[0][r] * scale) * sfg;
                     }
                 }
-                if constexpr (!HEAD) {  // y of the earlier launches; rows past H read nothing
-                    const int nr = a.H - oy;
-                    const float* po = a.out + (static_cast<size_t>(to - a.out_buf_t0) * a.H + oy) * a.pitch + ox + lane;
+                if constexpr (!HEAD) {  // y of the earlier launches (zero-filled past the edge)
 #pragma unroll
-                    for (int r = 0; r < BR; ++r)
-                        if (r < nr && ox + lane < a.W) v[r] += po[static_cast<size_t>(r) * a.pitch];
+                    for (int r = 0; r < BR; ++r) v[r] += opv[NOP - 1][r];
                 }
                 // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
                 float* ost = slab + NOP * SLAB;
