@@ -94,6 +94,23 @@
 #ifndef SFK_RS_RAWFENCE
 #define SFK_RS_RAWFENCE 1
 #endif
+// SFK_RS_PSPLIT=1: the three halo boxes of a plane are issued by lane 0 of
+// the last three A warps (one box each; the x box carries the expect_tx of
+// all three) instead of one thread issuing all three: the issue (~1000
+// cycles per plane) leaves warp 0, which also runs two x-pass blocks.
+// Measured 206.4 us per c1 launch against 213.5 (timeline: warp 0's issue +
+// loop 996 -> 339 cycles per plane), so on.
+#ifndef SFK_RS_PSPLIT
+#define SFK_RS_PSPLIT 1
+#endif
+// SFK_RS_CPA=1 (WIDE): each B warp fetches the S^p / F rows of its own
+// outputs with cp.async (LSU path) one emitted plane ahead, which takes the
+// operand tiles off the per-SM TMA unit (it then carries only the halo
+// boxes and the y store). Measured 242 us against 206 (B waits ~1500 cycles
+// per plane for the copies), so off.
+#ifndef SFK_RS_CPA
+#define SFK_RS_CPA 0
+#endif
 
 namespace sfk {
 
@@ -289,7 +306,41 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             prodq.next();
         };
         constexpr int PROD = SFK_RS_PRODUCER;
-        if (tid == PROD) {
+        constexpr bool PSPLIT = SFK_RS_PSPLIT != 0;
+        // PSPLIT: box `pbox` of every plane is issued by lane 0 of warp
+        // NWA - 3 + pbox, each with its own copy of the plane cursor
+        const int pbox = (tid >> 5) - (NWA - 3);
+        const bool pissuer = PSPLIT && (tid & 31) == 0 && pbox >= 0;
+        PlaneStream pq;
+        int pcount = 0;
+        auto issue_box = [&]() {
+            while (!pq.done) {
+                const int tg = a.out_t0 + pq.p;
+                if (tg >= 0 && tg < a.T) break;
+                pq.next();
+            }
+            if (pq.done) return;
+            const int tg = a.out_t0 + pq.p;
+            const int s = pcount % STAGES;
+            float* dst = raw + static_cast<size_t>(s) * 3 * FB;
+            uint64_t* bar = &raw_full[s];
+            const int bx = pq.tile_x * TX - G::HX, by = pq.tile_y * TY - R, bt = tg - a.buf_t0;
+            if (pbox == 0) {
+                mbar_arrive_expect_tx(bar, 3 * BH * BW * sizeof(float));
+                tma_load_3d(dst, &a.tm_x, bar, bx, by, bt);
+            } else if (pbox == 1) {
+                tma_load_3d(dst + FB, &a.tm_sp, bar, bx, by, bt);
+            } else {
+                tma_load_3d(dst + 2 * FB, &a.tm_f[0], bar, bx, by, bt);
+            }
+            ++pcount;
+            pq.next();
+        };
+        if (pissuer) {
+            pq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            for (int s = 0; s < STAGES; ++s) issue_box();
+        }
+        if (!PSPLIT && tid == PROD) {
             prodq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
             prod_count = 0;
             for (int s = 0; s < STAGES; ++s) issue_next();
@@ -388,9 +439,13 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
             if (tid == 0) SFK_T(cnt, 4);
-            if (tid == PROD) {
+            if (!PSPLIT && tid == PROD) {
                 if (SFK_RS_RAWFENCE) fence_proxy_async();  // generic reads of stage s before the TMA overwrite
                 issue_next();
+            }
+            if (pissuer) {
+                fence_proxy_async();
+                issue_box();
             }
             ++cnt;
         }
@@ -677,7 +732,28 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             eq.next();
         };
         constexpr bool LSU = LSU_MODE;
-        if ((WIDE ? bt == 0 : lane == 0) && !(SFK_RS_EXP & 16) && !LSU && !SPX) {
+        constexpr bool CPA = WIDE && SFK_RS_CPA != 0;
+        PlaneStream cq;  // CPA: every B thread's cursor over the emitted planes
+        auto issue_cpa = [&]() {
+            if (cq.done) return;
+            const int t = a.out_t0 + cq.p - a.buf_t0, x0 = cq.tile_x * TX, y0 = cq.tile_y * TY + BR * wb;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ch = lane + 32 * j;  // 16-byte chunk: field ch / 64, row (ch % 64) / 8, float4 ch % 8
+                const int fld = ch >> 6, row = (ch & 63) >> 3, c4 = ch & 7;
+                const float* base = fld ? a.f[0] : a.sp;
+                const bool in = y0 + row < a.H;
+                const float* src =
+                    in ? base + (static_cast<size_t>(t) * a.H + y0 + row) * a.pitch + x0 + 4 * c4 : base;
+                cp_async16(slab + fld * SLSTEP + row * TX + 4 * c4, src, in ? 16 : 0);
+            }
+            cp_async_commit();
+            cq.next();
+        };
+        if constexpr (CPA) {
+            cq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
+            issue_cpa();
+        } else if ((WIDE ? bt == 0 : lane == 0) && !(SFK_RS_EXP & 16) && !LSU && !SPX) {
             eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
             issue_slab();
         }
@@ -881,6 +957,18 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                         fv[r] = nf[r];
                     }
                     fetch();  // the next emitted plane's operands
+                } else if constexpr (CPA) {
+                    cp_async_wait0();
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        spv[r] = slab[r * TX + lane];
+                        fv[r] = slab[SLSTEP + r * TX + lane];
+                    }
+                    __syncwarp();
+                    issue_cpa();                      // the next emitted plane's rows of this warp
+                    if (bt == 0) bulk_wait_read0();  // the previous y tile store has read the staging
+                    named_bar_sync(3, NB);
                 } else if constexpr (WIDE) {
                     mbar_wait(sfull, ecnt & 1);
 #pragma unroll
