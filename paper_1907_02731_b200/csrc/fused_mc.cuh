@@ -128,9 +128,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
     uint64_t* slab_full = mbar + STAGES + 2 * NXB;  // [NWB]
 
     __shared__ IterState st;
-    __shared__ PlaneStream prodq;
     __shared__ PlaneStream slabq[NWB];
-    __shared__ int prod_count;
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
@@ -162,34 +160,36 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
         // A: TMA producer + x-pass (conv3d.cpp:88-101) with in-register products
         // =====================================================================
         setmaxnreg_dec<G::RA>();
-        auto issue_next = [&]() {
-            while (!prodq.done) {
-                const int tg = a.out_t0 + prodq.p;
+        // box `pbox` (0 .. NR-1) of every plane is issued by lane 0 of warp
+        // NWA - NR + pbox with its own plane cursor (warp 0 runs two x-pass
+        // blocks; one issuer for all boxes costs ~1000 cycles per plane,
+        // fused_rs.cuh SFK_RS_PSPLIT); box 0 carries the expect_tx of all
+        const int pbox = (tid >> 5) - (G::NWA - NR);
+        const bool pissuer = (tid & 31) == 0 && pbox >= 0;
+        PlaneStream pq;
+        int pcount = 0;
+        auto issue_box = [&]() {
+            while (!pq.done) {
+                const int tg = a.out_t0 + pq.p;
                 if (tg >= 0 && tg < a.T) break;
-                prodq.next();
+                pq.next();
             }
-            if (prodq.done) return;
-            const int tg = a.out_t0 + prodq.p;
-            const int s = prod_count % STAGES;
-            float* dst = raw + static_cast<size_t>(s) * NR * FB;
+            if (pq.done) return;
+            const int tg = a.out_t0 + pq.p;
+            const int s = pcount % STAGES;
+            float* dst = raw + static_cast<size_t>(s) * NR * FB + pbox * FB;
             uint64_t* bar = &raw_full[s];
-            mbar_arrive_expect_tx(bar, NR * BH * BW * sizeof(float));
-            const int bx = prodq.tile_x * TX - G::HX, by = prodq.tile_y * TY - R, bt = tg - a.buf_t0;
-            tma_load_3d(dst, &a.tm_x, bar, bx, by, bt);
-            if constexpr (HEAD) {
-                tma_load_3d(dst + FB, &a.tm_sp, bar, bx, by, bt);
-                tma_load_3d(dst + 2 * FB, &a.tm_f[0], bar, bx, by, bt);
-            } else {
-#pragma unroll
-                for (int i = 0; i < NF; ++i) tma_load_3d(dst + (1 + i) * FB, &a.tm_f[i], bar, bx, by, bt);
-            }
-            ++prod_count;
-            prodq.next();
+            const int bx = pq.tile_x * TX - G::HX, by = pq.tile_y * TY - R, bt = tg - a.buf_t0;
+            if (pbox == 0) mbar_arrive_expect_tx(bar, NR * BH * BW * sizeof(float));
+            const CUtensorMap* map = pbox == 0 ? &a.tm_x : HEAD ? (pbox == 1 ? &a.tm_sp : &a.tm_f[0])
+                                                               : &a.tm_f[pbox - 1];
+            tma_load_3d(dst, map, bar, bx, by, bt);
+            ++pcount;
+            pq.next();
         };
-        if (tid == 0) {
-            prodq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
-            prod_count = 0;
-            for (int s = 0; s < STAGES; ++s) issue_next();
+        if (pissuer) {
+            pq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+            for (int s = 0; s < STAGES; ++s) issue_box();
         }
         const bool sigm = HEAD && st.mode == 2;
         const int xw = tid >> 5, xl = tid & 31;  // lane -> (row xl & 7, strip xl >> 3)
@@ -282,9 +282,9 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
             }
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
-            if (tid == 0) {
+            if (pissuer) {
                 fence_proxy_async();  // generic reads of stage s before the TMA overwrite
-                issue_next();
+                issue_box();
             }
             ++cnt;
         }
