@@ -46,7 +46,10 @@ enum sfseg_status {
     SFSEG_ERR_DEGENERATE = 4, /* DegenerateSolutionError (engine.cpp:174-175) */
     SFSEG_ERR_CAPACITY = 5,   /* CapacityError           (device memory exhausted) */
     SFSEG_ERR_CUDA = 6,       /* Error                   (CUDA runtime/driver failure) */
-    SFSEG_ERR_STATE = 7       /* Error                   (API misuse, e.g. solve before load) */
+    SFSEG_ERR_STATE = 7,      /* Error                   (API misuse, e.g. solve before load) */
+    SFSEG_ERR_IO = 8,         /* IoError                 (volume.cpp:143-144, open failure) */
+    SFSEG_ERR_FORMAT = 9,     /* FormatError             (volume.cpp:151-166, header) */
+    SFSEG_ERR_CORRUPTION = 10 /* CorruptionError         (volume.cpp:147-148, 171-173, truncation) */
 };
 
 /* Arithmetic contract of the stencil kernels.
@@ -146,6 +149,20 @@ void* sfseg_ctx_stream(sfseg_ctx* ctx);
 int sfseg_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
                int32_t channels, const float* unary, const float* const* pairwise,
                const float* x0, int32_t mem);
+
+/* sfseg_load from SFSV volume containers (the reference's load_volume,
+ * volume.cpp:142-184: 32-byte little-endian header "SFSV", version 1, T/H/W,
+ * one channel, f32 payload). Every header is checked before any payload
+ * moves; payloads stream from the file through two pinned host buffers into
+ * the device (file reads overlap the DMA), and the non-finite / sign checks
+ * of FeatureSet::validate run on the device. Errors follow load_volume:
+ * SFSEG_ERR_IO (cannot open), SFSEG_ERR_CORRUPTION (short header or
+ * truncated payload), SFSEG_ERR_FORMAT (magic, version, dtype, reserved
+ * bytes, channel count), SFSEG_ERR_VALIDATION (empty axis, non-finite or
+ * negative unary values); SFSEG_ERR_SHAPE when the files disagree in shape
+ * (volume.cpp:90-91). x0_path may be NULL. */
+int sfseg_load_files(sfseg_ctx* ctx, const char* unary_path, const char* const* pairwise_paths,
+                     int32_t channels, const char* x0_path);
 
 /* Runs iterations first_iter..last_iter (1-based, inclusive) of Algorithm 1
  * on the resident problem. first_iter == 1 restarts from S or x0; otherwise

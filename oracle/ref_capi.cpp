@@ -39,6 +39,9 @@ int fail(const std::exception& e, int code) {
     catch (const sfseg::ShapeError& e) { return fail(e, SFSEG_ERR_SHAPE); }         \
     catch (const sfseg::ValidationError& e) { return fail(e, SFSEG_ERR_VALIDATION); } \
     catch (const sfseg::DegenerateSolutionError& e) { return fail(e, SFSEG_ERR_DEGENERATE); } \
+    catch (const sfseg::IoError& e) { return fail(e, SFSEG_ERR_IO); }               \
+    catch (const sfseg::FormatError& e) { return fail(e, SFSEG_ERR_FORMAT); }       \
+    catch (const sfseg::CorruptionError& e) { return fail(e, SFSEG_ERR_CORRUPTION); } \
     catch (const std::exception& e) { return fail(e, SFSEG_ERR_STATE); }
 
 sfseg::SfsegConfig to_cfg(const sfseg_params* p, int threads) {
@@ -81,6 +84,26 @@ sfseg::FeatureSet features(uint32_t T, uint32_t H, uint32_t W, int32_t C, const 
 extern "C" {
 
 const char* sfref_last_error(void) { return g_msg; }
+
+// SFSV containers through the reference's own writer / reader
+// (volume.cpp:117-184): fixtures and error-code parity for sfseg_load_files
+int sfref_save_volume(const char* path, uint32_t T, uint32_t H, uint32_t W, const float* d) {
+    REF_TRY
+    sfseg::save_volume(vol(T, H, W, d, sfseg::VolumeRole::generic), path);
+    return 0;
+    REF_CATCH
+}
+
+int sfref_load_volume(const char* path, uint32_t* dims, float* out, size_t cap) {
+    REF_TRY
+    const sfseg::FeatureVolume v = sfseg::load_volume(path);
+    dims[0] = v.shape().frames;
+    dims[1] = v.shape().height;
+    dims[2] = v.shape().width;
+    if (out && cap >= v.size()) std::memcpy(out, v.data(), v.size() * sizeof(float));
+    return 0;
+    REF_CATCH
+}
 
 int sfref_validate(const sfseg_params* p) {
     REF_TRY

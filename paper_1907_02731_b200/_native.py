@@ -23,6 +23,9 @@ SFSEG_ERR_DEGENERATE = 4
 SFSEG_ERR_CAPACITY = 5
 SFSEG_ERR_CUDA = 6
 SFSEG_ERR_STATE = 7
+SFSEG_ERR_IO = 8
+SFSEG_ERR_FORMAT = 9
+SFSEG_ERR_CORRUPTION = 10
 
 SFSEG_ARITH_EXACT = 0
 SFSEG_ARITH_FAST = 1
@@ -59,6 +62,18 @@ class CudaError(Error):
     pass
 
 
+class IoError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class CorruptionError(Error):
+    pass
+
+
 _EXC = {
     SFSEG_ERR_PARAMETER: ParameterError,
     SFSEG_ERR_SHAPE: ShapeError,
@@ -67,6 +82,9 @@ _EXC = {
     SFSEG_ERR_CAPACITY: CapacityError,
     SFSEG_ERR_CUDA: CudaError,
     SFSEG_ERR_STATE: Error,
+    SFSEG_ERR_IO: IoError,
+    SFSEG_ERR_FORMAT: FormatError,
+    SFSEG_ERR_CORRUPTION: CorruptionError,
 }
 
 
@@ -143,6 +161,7 @@ _SIGS = {
     "sfseg_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "sfseg_ctx_stream": (C.c_void_p, [_P]),
     "sfseg_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, _I32]),
+    "sfseg_load_files": (C.c_int, [_P, C.c_char_p, _P, _I32, C.c_char_p]),
     "sfseg_solve": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, C.POINTER(IterRecord)]),
     "sfseg_solve_until": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, _I32, C.c_double,
                                     C.POINTER(C.c_int32), C.POINTER(IterRecord)]),

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -450,6 +451,8 @@ struct sfseg_ctx {
     long long sched_key = -1;
     // generic-path temporaries (allocated lazily)
     std::vector<float*> tmp;
+    void* pin[2] = {nullptr, nullptr};  // sfseg_load_files: pinned file-read buffers
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     float* q = nullptr;              // Q = sum_c f_c^2 of the channel set q_for (fused_mc.cuh)
     std::vector<float*> q_for;
     // dense staging for host transfers (one contiguous DMA, re-pitched on the
@@ -1121,6 +1124,113 @@ void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
     c->q_for.clear();  // channel contents changed
 }
 
+// ---- SFSV containers (load_volume, volume.cpp:142-184) ---------------------
+
+constexpr size_t kPinChunk = size_t(32) << 20;  // bytes per pinned buffer
+
+struct SfsvFile {
+    std::FILE* f = nullptr;
+    uint32_t T = 0, H = 0, W = 0;
+    ~SfsvFile() {
+        if (f) std::fclose(f);
+    }
+};
+
+uint32_t get_u32_le(const unsigned char* b) {
+    return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+}
+
+// header checks in load_volume's order (volume.cpp:143-166)
+void open_sfsv(const char* path, SfsvFile& sf) {
+    if (!path) fail(SFSEG_ERR_PARAMETER, "null path");
+    const std::string p(path);
+    sf.f = std::fopen(path, "rb");
+    if (!sf.f) fail(SFSEG_ERR_IO, "cannot open for reading: " + p);
+    unsigned char h[32];
+    if (std::fread(h, 1, sizeof h, sf.f) != sizeof h)
+        fail(SFSEG_ERR_CORRUPTION, "file shorter than the container header: " + p);
+    if (std::memcmp(h, "SFSV", 4) != 0) fail(SFSEG_ERR_FORMAT, "bad magic, not a volume container: " + p);
+    if (get_u32_le(h + 4) != 1u) fail(SFSEG_ERR_FORMAT, "unsupported container version in " + p);
+    sf.T = get_u32_le(h + 8);
+    sf.H = get_u32_le(h + 12);
+    sf.W = get_u32_le(h + 16);
+    const uint32_t channels = get_u32_le(h + 20);
+    if (h[24] != 0x01) fail(SFSEG_ERR_FORMAT, "unsupported payload dtype in " + p);
+    for (int i = 25; i < 32; ++i)
+        if (h[i] != 0) fail(SFSEG_ERR_FORMAT, "reserved header bytes set in " + p);
+    if (channels != 1)
+        fail(SFSEG_ERR_FORMAT, "expected a single-channel container, got " + std::to_string(channels) +
+                                   " channels in " + p);
+    check_shape(sf.T, sf.H, sf.W);
+}
+
+// payload -> dense device staging through two pinned buffers (the read of
+// chunk k overlaps the DMA of chunk k - 1), then re-pitched into dst. The
+// payload is little-endian f32, the host's own layout on x86-64 / aarch64.
+void stream_sfsv(sfseg_ctx* c, SfsvFile& sf, const char* path, float* dst) {
+    for (int b = 0; b < 2; ++b)
+        if (!c->pin[b]) {
+            ck(cudaHostAlloc(&c->pin[b], kPinChunk, cudaHostAllocDefault), "cudaHostAlloc");
+            ck(cudaEventCreateWithFlags(&c->pin_ev[b], cudaEventDisableTiming), "event");
+        }
+    const size_t rows = static_cast<size_t>(c->T) * c->H;
+    const size_t bytes = rows * c->W * sizeof(float);
+    char* dense = reinterpret_cast<char*>(c->P == c->W ? dst : stage_buf(c));
+    bool used[2] = {false, false};
+    for (size_t off = 0, k = 0; off < bytes; off += kPinChunk, ++k) {
+        const int b = static_cast<int>(k & 1);
+        const size_t n = std::min(kPinChunk, bytes - off);
+        if (used[b]) ck(cudaEventSynchronize(c->pin_ev[b]), "pinned buffer");  // its DMA is done
+        if (std::fread(c->pin[b], 1, n, sf.f) != n)
+            fail(SFSEG_ERR_CORRUPTION, std::string("payload truncated in ") + path);
+        ck(cudaMemcpyAsync(dense + off, c->pin[b], n, cudaMemcpyHostToDevice, c->stream), "upload file");
+        ck(cudaEventRecord(c->pin_ev[b], c->stream), "event");
+        used[b] = true;
+    }
+    if (c->P != c->W) {
+        sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(reinterpret_cast<float*>(dense), c->W, dst,
+                                                             c->P, rows, c->W);
+        launched(c->stream, "k_repitch");
+    }
+}
+
+void load_files_impl(sfseg_ctx* c, const char* unary, const char* const* pairwise, int32_t C,
+                     const char* x0) {
+    if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
+    if (!pairwise) fail(SFSEG_ERR_PARAMETER, "null pairwise path list");
+    std::vector<SfsvFile> files(static_cast<size_t>(C) + 1 + (x0 ? 1 : 0));
+    open_sfsv(unary, files[0]);
+    for (int i = 0; i < C; ++i) open_sfsv(pairwise[i], files[1 + i]);
+    if (x0) open_sfsv(x0, files[1 + C]);
+    for (size_t i = 1; i < files.size(); ++i)
+        if (files[i].T != files[0].T || files[i].H != files[0].H || files[i].W != files[0].W)
+            fail(SFSEG_ERR_SHAPE, i <= static_cast<size_t>(C)
+                                      ? "pairwise channel shape differs from unary shape"
+                                      : "x0 shape differs from the feature shape");
+    set_shape(c, files[0].T, files[0].H, files[0].W, C);
+    if (c->guard_applied)
+        for (size_t i = 0; i < c->Fw.size(); ++i)
+            if (c->Fw[i] != c->F[i]) dfree(c->Fw[i]);
+    c->Fw = c->F;
+    c->guard_applied = false;
+    c->sp_p = NAN;
+    c->cur = -1;
+    c->resident = false;
+    stream_sfsv(c, files[0], unary, c->S);
+    for (int i = 0; i < C; ++i) stream_sfsv(c, files[1 + i], pairwise[i], c->F[i]);
+    c->has_x0 = x0 != nullptr;
+    if (x0) {
+        if (!c->x0) c->x0 = dalloc_vol(c);
+        stream_sfsv(c, files[1 + C], x0, c->x0);
+    }
+    // load_volume rejects non-finite payloads; FeatureSet::validate the signs
+    validate_vol(c, c->S, true, "unary");
+    for (int i = 0; i < C; ++i) validate_vol(c, c->F[i], false, "pairwise");
+    if (x0) validate_vol(c, c->x0, true, "x0");
+    c->resident = true;
+    c->q_for.clear();
+}
+
 // stateless helpers: (re)use the resident buffers of a scratch problem
 void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
     check_shape(T, H, W);
@@ -1264,6 +1374,10 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         cudaFree(c->acc3);
         cudaFree(c->cnt2);
         cudaFree(c->ticket);
+        for (int b = 0; b < 2; ++b) {
+            if (c->pin[b]) cudaFreeHost(c->pin[b]);
+            if (c->pin_ev[b]) cudaEventDestroy(c->pin_ev[b]);
+        }
         if (c->conv_part) cudaFree(c->conv_part);
         if (c->st_prev) cudaFree(c->st_prev);
         if (c->norms) cudaFree(c->norms);
@@ -1325,6 +1439,16 @@ int sfseg_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         load_impl(c, T, H, W, C, S, F, x0, mem);
+    });
+}
+
+int sfseg_load_files(sfseg_ctx* c, const char* unary, const char* const* pairwise, int32_t C,
+                     const char* x0) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        load_files_impl(c, unary, pairwise, C, x0);
     });
 }
 

@@ -34,15 +34,16 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 from . import _native as N
-from ._native import (CapacityError, DegenerateSolutionError, Error, ParameterError,
-                      ShapeError, ValidationError)
+from ._native import (CapacityError, CorruptionError, DegenerateSolutionError, Error,
+                      FormatError, IoError, ParameterError, ShapeError, ValidationError)
 
 __all__ = [
     "KernelConfig", "SfsegConfig", "FeatureSet", "IterationRecord", "RunTrace", "RunResult",
     "SeparableKernel3D", "make_gaussian_kernel", "convolve_separable", "sfseg_step",
     "sfseg_step_channel", "normalize_l2", "project_binary", "threshold_final", "run",
     "separable_convolution_count", "Context", "default_context", "Error", "ParameterError",
-    "ShapeError", "ValidationError", "DegenerateSolutionError", "CapacityError",
+    "ShapeError", "ValidationError", "DegenerateSolutionError", "CapacityError", "IoError",
+    "FormatError", "CorruptionError", "run_files", "volume_shape",
 ]
 
 ARITH_EXACT = N.SFSEG_ARITH_EXACT
@@ -534,3 +535,43 @@ def run_until_converged(features: FeatureSet, cfg: SfsegConfig, tol: float,
         ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
         N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold), ob.ptr, mb.ptr, mem))
     return RunResult(soft, mask, trace), done.value
+
+
+def volume_shape(path) -> tuple:
+    """(T, H, W) from an SFSV container header (volume.hpp:111-121)."""
+    with open(path, "rb") as f:
+        h = f.read(32)
+    if len(h) < 32:
+        raise CorruptionError(f"file shorter than the container header: {path}")
+    return tuple(int.from_bytes(h[o:o + 4], "little") for o in (8, 12, 16))
+
+
+def run_files(unary_path, pairwise_paths: Sequence, cfg: SfsegConfig, x0_path=None,
+              ctx: Optional[Context] = None) -> RunResult:
+    """run() on volumes stored as SFSV containers (load_volume,
+    volume.cpp:142-184), streamed from the files into device memory by
+    sfseg_load_files (two pinned buffers, reads overlapped with the DMA);
+    the files' headers are checked first and load_volume's errors surface
+    as IoError / FormatError / CorruptionError / ValidationError."""
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    paths = [os.fsencode(x) for x in pairwise_paths]
+    arr = (C.c_char_p * max(1, len(paths)))(*paths)
+    lib = ctx._lib
+    trace = RunTrace()
+    recs = (N.IterRecord * cfg.iterations)()
+    with ctx.lock:
+        N.check(lib.sfseg_load_files(ctx.handle, os.fsencode(unary_path), C.cast(arr, C.c_void_p),
+                                     len(paths), os.fsencode(x0_path) if x0_path else None))
+        T, H, W = volume_shape(unary_path)
+        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, cfg.iterations, recs))
+        for r in recs:
+            trace.iterations.append(IterationRecord(r.iter, r.l2_norm_pre_normalize,
+                                                    wall_time_s=r.wall_time_s))
+        soft = np.empty((T, H, W), np.float32)
+        mask = np.empty((T, H, W), np.uint8)
+        N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold),
+                                   soft.ctypes.data_as(C.c_void_p), mask.ctypes.data_as(C.c_void_p),
+                                   N.SFSEG_MEM_HOST))
+    return RunResult(soft, mask, trace)

@@ -206,6 +206,19 @@ class Reference(_Base):
             C.c_int32(len(ck)), _vp(ck_out) if len(ck) else None))
         return soft, mask, norms, ck_out
 
+    def save_volume(self, path, v):
+        """sfseg_ref::save_volume (volume.cpp:117-140)"""
+        v = np.ascontiguousarray(v, _F)
+        T, H, W = v.shape
+        self._chk(self.lib.sfref_save_volume(str(path).encode(), C.c_uint32(T), C.c_uint32(H),
+                                             C.c_uint32(W), _vp(v)))
+
+    def load_volume_rc(self, path):
+        """sfseg_ref::load_volume (volume.cpp:142-184): (status, (T, H, W) or None)"""
+        dims = (C.c_uint32 * 3)()
+        rc = self.lib.sfref_load_volume(str(path).encode(), dims, None, C.c_size_t(0))
+        return rc, (tuple(int(d) for d in dims) if rc == 0 else None)
+
     def global_loop(self, S, F, cfg, iterations, threads=1):
         S = np.ascontiguousarray(S, _F)
         F = [np.ascontiguousarray(f, _F) for f in F]
