@@ -453,6 +453,7 @@ struct sfseg_ctx {
     std::vector<float*> tmp;
     void* pin[2] = {nullptr, nullptr};  // sfseg_load_files: pinned file-read buffers
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    bool pin_used[2] = {false, false};  // pin_ev[b] marks a DMA still reading pin[b]
     float* q = nullptr;              // Q = sum_c f_c^2 of the channel set q_for (fused_mc.cuh)
     std::vector<float*> q_for;
     // dense staging for host transfers (one contiguous DMA, re-pitched on the
@@ -1176,16 +1177,16 @@ void stream_sfsv(sfseg_ctx* c, SfsvFile& sf, const char* path, float* dst) {
     const size_t rows = static_cast<size_t>(c->T) * c->H;
     const size_t bytes = rows * c->W * sizeof(float);
     char* dense = reinterpret_cast<char*>(c->P == c->W ? dst : stage_buf(c));
-    bool used[2] = {false, false};
     for (size_t off = 0, k = 0; off < bytes; off += kPinChunk, ++k) {
         const int b = static_cast<int>(k & 1);
         const size_t n = std::min(kPinChunk, bytes - off);
-        if (used[b]) ck(cudaEventSynchronize(c->pin_ev[b]), "pinned buffer");  // its DMA is done
+        // the previous DMA out of this buffer (this file's or an earlier one's) is done
+        if (c->pin_used[b]) ck(cudaEventSynchronize(c->pin_ev[b]), "pinned buffer");
         if (std::fread(c->pin[b], 1, n, sf.f) != n)
             fail(SFSEG_ERR_CORRUPTION, std::string("payload truncated in ") + path);
         ck(cudaMemcpyAsync(dense + off, c->pin[b], n, cudaMemcpyHostToDevice, c->stream), "upload file");
         ck(cudaEventRecord(c->pin_ev[b], c->stream), "event");
-        used[b] = true;
+        c->pin_used[b] = true;
     }
     if (c->P != c->W) {
         sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(reinterpret_cast<float*>(dense), c->W, dst,
