@@ -309,6 +309,39 @@ int sfseg_shard_norms(sfseg_ctx* ctx, int32_t count, double* norms);
 /* Soft iterate / mask of the rank's output frames; frac as threshold_final. */
 int sfseg_shard_download(sfseg_ctx* ctx, double frac, float* soft, uint8_t* mask, int32_t mem);
 
+/* ---- explicit-affinity oracle on the GPU (oracle.hpp:76-107) -------------
+ * Matrix-free fp64 versions of the reference's SparseAffinity path: every
+ * entry M_ij = sp_i sp_j pair(i,j) G(j-i) is regenerated in the reference's
+ * order and rounding (oracle.cpp:137-166; S^p with the host's std::pow), rows
+ * summed in ascending column order (oracle.cpp:191-207). The Taylor kinds are
+ * bit-identical to the reference's matvec; EXACT differs only by the device
+ * exp. No kOracleMaxNodes cap (oracle.hpp:25): volumes of any size that fit
+ * the device. Channels: 1..8. Errors as build_affinity_* / power_iteration:
+ * SFSEG_ERR_VALIDATION (features, the [0,1] guard), SFSEG_ERR_PARAMETER
+ * (config, max_iters < 1, zero x0), SFSEG_ERR_DEGENERATE (M x = 0). */
+enum sfseg_affinity_kind {
+    SFSEG_AFFINITY_EXACT = 0,              /* build_affinity_exact             */
+    SFSEG_AFFINITY_TAYLOR = 1,             /* build_affinity_taylor            */
+    SFSEG_AFFINITY_TAYLOR_CHANNEL_SUM = 2  /* build_affinity_taylor_channel_sum */
+};
+
+/* y = M x (matvec, oracle.cpp:191-207); x and y are fp64 volumes. */
+int sfseg_affinity_matvec(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                          int32_t channels, const float* unary, const float* const* pairwise,
+                          const sfseg_params* p, int32_t kind, const double* x, double* y,
+                          int32_t mem);
+
+/* power_iteration (oracle.cpp:219-247) from x0 until ||x_k+1 - x_k|| < tol or
+ * max_iters, then eigenvalue = cluster_score (oracle.cpp:249-258). Norms and
+ * dot products are fixed-order fp64 tree sums (the reference sums
+ * sequentially), so results agree to ~1e-15 relative, independent of run. */
+int sfseg_affinity_power_iteration(sfseg_ctx* ctx, uint32_t frames, uint32_t height,
+                                   uint32_t width, int32_t channels, const float* unary,
+                                   const float* const* pairwise, const sfseg_params* p,
+                                   int32_t kind, const double* x0, int32_t max_iters, double tol,
+                                   double* eigenvector, double* eigenvalue,
+                                   int32_t* iterations_used, int32_t mem);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@
 #include "sfseg/engine.hpp"
 #include "sfseg/errors.hpp"
 #include "sfseg/metrics.hpp"
+#include "sfseg/oracle.hpp"
 #include "sfseg/rng.hpp"
 #include "sfseg/volume.hpp"
 
@@ -42,6 +43,7 @@ int fail(const std::exception& e, int code) {
     catch (const sfseg::IoError& e) { return fail(e, SFSEG_ERR_IO); }               \
     catch (const sfseg::FormatError& e) { return fail(e, SFSEG_ERR_FORMAT); }       \
     catch (const sfseg::CorruptionError& e) { return fail(e, SFSEG_ERR_CORRUPTION); } \
+    catch (const sfseg::CapacityError& e) { return fail(e, SFSEG_ERR_CAPACITY); }   \
     catch (const std::exception& e) { return fail(e, SFSEG_ERR_STATE); }
 
 sfseg::SfsegConfig to_cfg(const sfseg_params* p, int threads) {
@@ -84,6 +86,39 @@ sfseg::FeatureSet features(uint32_t T, uint32_t H, uint32_t W, int32_t C, const 
 extern "C" {
 
 const char* sfref_last_error(void) { return g_msg; }
+
+// explicit-matrix oracle (oracle.cpp:67-258): pins sfseg_affinity_*
+namespace {
+sfseg::SparseAffinity ref_affinity(int32_t kind, const sfseg::FeatureSet& fs, const sfseg::SfsegConfig& c) {
+    if (kind == 0) return sfseg::build_affinity_exact(fs, c);
+    if (kind == 1) return sfseg::build_affinity_taylor(fs, c);
+    return sfseg::build_affinity_taylor_channel_sum(fs, c);
+}
+}  // namespace
+
+int sfref_affinity_matvec(uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+                          const float* const* F, const sfseg_params* p, int32_t kind, const double* x,
+                          double* y) {
+    REF_TRY
+    const auto m = ref_affinity(kind, features(T, H, W, C, S, F), to_cfg(p, 1));
+    const std::vector<double> r = sfseg::matvec(m, std::span<const double>(x, m.size()), 1);
+    std::memcpy(y, r.data(), r.size() * sizeof(double));
+    return 0;
+    REF_CATCH
+}
+
+int sfref_power_iteration(uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+                          const float* const* F, const sfseg_params* p, int32_t kind, const double* x0,
+                          int32_t max_iters, double tol, double* vec, double* value, int32_t* used) {
+    REF_TRY
+    const auto m = ref_affinity(kind, features(T, H, W, C, S, F), to_cfg(p, 1));
+    const auto r = sfseg::power_iteration(m, std::vector<double>(x0, x0 + m.size()), max_iters, tol, 1);
+    std::memcpy(vec, r.eigenvector.data(), r.eigenvector.size() * sizeof(double));
+    *value = r.eigenvalue;
+    *used = r.iterations_used;
+    return 0;
+    REF_CATCH
+}
 
 // SFSV containers through the reference's own writer / reader
 // (volume.cpp:117-184): fixtures and error-code parity for sfseg_load_files

@@ -32,6 +32,7 @@ SFSEG_ARITH_FAST = 1
 SFSEG_MEM_HOST = 0
 SFSEG_MEM_DEVICE = 1
 SFSEG_CONV_STEP, SFSEG_CONV_ANGLE = 0, 1  # enum sfseg_conv
+SFSEG_AFFINITY_EXACT, SFSEG_AFFINITY_TAYLOR, SFSEG_AFFINITY_TAYLOR_CHANNEL_SUM = 0, 1, 2
 
 
 class Error(RuntimeError):
@@ -162,6 +163,11 @@ _SIGS = {
     "sfseg_ctx_stream": (C.c_void_p, [_P]),
     "sfseg_load": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, _I32]),
     "sfseg_load_files": (C.c_int, [_P, C.c_char_p, _P, _I32, C.c_char_p]),
+    "sfseg_affinity_matvec": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, C.POINTER(Params), _I32,
+                                        _P, _P, _I32]),
+    "sfseg_affinity_power_iteration": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P,
+                                                 C.POINTER(Params), _I32, _P, _I32, C.c_double, _P,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_int32), _I32]),
     "sfseg_solve": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, C.POINTER(IterRecord)]),
     "sfseg_solve_until": (C.c_int, [_P, C.POINTER(Params), _I32, _I32, _I32, C.c_double,
                                     C.POINTER(C.c_int32), C.POINTER(IterRecord)]),

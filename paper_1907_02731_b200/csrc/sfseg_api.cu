@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -26,6 +27,7 @@
 #include "fused_ws.cuh"
 #include "fused_rs.cuh"
 #include "fused_mc.cuh"
+#include "affinity.cuh"
 
 namespace {
 
@@ -1326,6 +1328,209 @@ const char* sfseg_last_error(void) { return g_err.c_str(); }
 
 const char* sfseg_build_info(void) {
     return "sfseg_cuda abi=" "1" " arch=sm_100a fused=exact(rt,r)={(1,2),(1,3),(2,4),(2,5)}";
+}
+
+// ---- explicit-affinity oracle on the GPU (oracle.cpp:67-258, affinity.cuh) ----
+}  // extern "C"
+
+namespace {
+
+struct DBuf {  // owning device allocation for one call
+    void* p = nullptr;
+    explicit DBuf(size_t bytes) { ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct AffProblem {
+    std::vector<std::unique_ptr<DBuf>> bufs;
+    sfk::AffArgs a{};
+    long long n = 0;
+    cudaStream_t stream = nullptr;
+    int nb = 0;
+    DBuf* parts = nullptr;
+    DBuf* scal = nullptr;  // [0] norm, [1] second scalar
+    template <class T> T* alloc(size_t count) {
+        bufs.push_back(std::make_unique<DBuf>(count * sizeof(T)));
+        return bufs.back()->as<T>();
+    }
+};
+
+// build_affinity_impl's checks (oracle.cpp:69-86, minus the node cap) and
+// the device-side operands: dense float channels, S^p in fp64 (host std::pow,
+// the reference's own libm), fp64 taps of make_gaussian_kernel
+void aff_setup(sfseg_ctx* c, AffProblem& P, uint32_t T, uint32_t H, uint32_t W, int32_t C,
+               const float* S, const float* const* F, const sfseg_params* p, int32_t kind,
+               int32_t mem) {
+    validate_params(p);
+    check_shape(T, H, W);
+    if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
+    if (C > 8) fail(SFSEG_ERR_CAPACITY, "the GPU affinity oracle takes at most 8 channels");
+    if (kind < SFSEG_AFFINITY_EXACT || kind > SFSEG_AFFINITY_TAYLOR_CHANNEL_SUM)
+        fail(SFSEG_ERR_PARAMETER, "unknown affinity kind");
+    if (!S || !F) fail(SFSEG_ERR_PARAMETER, "null input");
+    const HostKernel k = make_kernel(p->radii, p->sigmas);
+    if (k.rt > 31 || k.ry > 31 || k.rx > 31) fail(SFSEG_ERR_CAPACITY, "kernel radius above 31");
+    const size_t n = static_cast<size_t>(T) * H * W;
+    P.n = static_cast<long long>(n);
+    P.stream = c->stream;
+    // host copies for validation and S^p (device inputs come down once)
+    auto host_of = [&](const float* src) {
+        std::vector<float> h(n);
+        ck(cudaMemcpy(h.data(), src, n * sizeof(float),
+                      mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost),
+           "copy");
+        return h;
+    };
+    const std::vector<float> hs = host_of(S);
+    for (float v : hs) {  // FeatureSet::validate (volume.cpp:72-93)
+        if (!std::isfinite(v)) fail(SFSEG_ERR_VALIDATION, "unary contains a non-finite value");
+        if (v < 0.0f) fail(SFSEG_ERR_VALIDATION, "unary/solution volume contains a negative value");
+    }
+    for (int ch = 0; ch < C; ++ch) {
+        if (!F[ch]) fail(SFSEG_ERR_PARAMETER, "null pairwise channel");
+        const std::vector<float> hf = host_of(F[ch]);
+        for (float v : hf) {
+            if (!std::isfinite(v)) fail(SFSEG_ERR_VALIDATION, "pairwise contains a non-finite value");
+            if (!p->allow_negative_affinity && (v < 0.0f || v > 1.0f))
+                fail(SFSEG_ERR_VALIDATION, "pairwise channel " + std::to_string(ch) +
+                                               " leaves [0,1]; prescale it or enable allow_negative_affinity");
+        }
+        float* d = P.alloc<float>(n);
+        ck(cudaMemcpyAsync(d, hf.data(), n * sizeof(float), cudaMemcpyHostToDevice, c->stream), "upload");
+        P.a.f[ch] = d;
+        ck(cudaStreamSynchronize(c->stream), "upload");  // hf goes out of scope
+    }
+    std::vector<double> sp(n);
+    for (size_t i = 0; i < n; ++i)
+        sp[i] = p->p == 0.0 ? 1.0 : std::pow(static_cast<double>(hs[i]), p->p);
+    double* dsp = P.alloc<double>(n);
+    ck(cudaMemcpy(dsp, sp.data(), n * sizeof(double), cudaMemcpyHostToDevice), "upload");
+    P.a.sp = dsp;
+    P.a.T = static_cast<int>(T);
+    P.a.H = static_cast<int>(H);
+    P.a.W = static_cast<int>(W);
+    P.a.C = C;
+    P.a.rt = k.rt;
+    P.a.ry = k.ry;
+    P.a.rx = k.rx;
+    P.a.exact = kind == SFSEG_AFFINITY_EXACT;
+    P.a.alpha = p->alpha;
+    P.a.base = kind == SFSEG_AFFINITY_TAYLOR_CHANNEL_SUM ? static_cast<double>(C) : 1.0;
+    for (int i = 0; i <= 2 * k.rt; ++i) P.a.tt[i] = k.t[i];
+    for (int i = 0; i <= 2 * k.ry; ++i) P.a.ty[i] = k.y[i];
+    for (int i = 0; i <= 2 * k.rx; ++i) P.a.tx[i] = k.x[i];
+    P.nb = c->num_sms * 4;
+    P.bufs.push_back(std::make_unique<DBuf>(P.nb * sizeof(double)));
+    P.parts = P.bufs.back().get();
+    P.bufs.push_back(std::make_unique<DBuf>(4 * sizeof(double)));
+    P.scal = P.bufs.back().get();
+}
+
+void aff_matvec(sfseg_ctx* c, AffProblem& P, const double* x, double* y) {
+    P.a.x = x;
+    P.a.y = y;
+    const int grid = static_cast<int>(std::min<long long>((P.n + 255) / 256, c->num_sms * 16LL));
+    sfk::k_affinity_matvec<<<grid, 256, 0, c->stream>>>(P.a);
+    launched(c->stream, "k_affinity_matvec");
+}
+
+// out = fixed-order fp64 sum (OP of k_dot_blocks), sqrt when asked
+template <int OP>
+void aff_sum(sfseg_ctx* c, AffProblem& P, const double* a, const double* b, const double* scale,
+             double* out, bool sq) {
+    sfk::k_dot_blocks<OP><<<P.nb, sfk::kRedThreads, 0, c->stream>>>(a, b, scale, P.n, P.parts->as<double>());
+    sfk::k_sum_final<<<1, 32, 0, c->stream>>>(P.parts->as<double>(), P.nb, out, sq ? 1 : 0);
+    launched(c->stream, "affinity reduction");
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfseg_affinity_matvec(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C,
+                          const float* S, const float* const* F, const sfseg_params* p, int32_t kind,
+                          const double* x, double* y, int32_t mem) {
+    return guarded([&] {
+        if (!c || !p || !x || !y) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        AffProblem P;
+        aff_setup(c, P, T, H, W, C, S, F, p, kind, mem);
+        const size_t n = static_cast<size_t>(P.n);
+        const double* dx = x;
+        double* dy = y;
+        if (mem != SFSEG_MEM_DEVICE) {
+            double* bx = P.alloc<double>(n);
+            ck(cudaMemcpyAsync(bx, x, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "upload x");
+            dx = bx;
+            dy = P.alloc<double>(n);
+        }
+        aff_matvec(c, P, dx, dy);
+        if (mem != SFSEG_MEM_DEVICE)
+            ck(cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "download y");
+        ck(cudaStreamSynchronize(c->stream), "matvec");
+    });
+}
+
+int sfseg_affinity_power_iteration(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C,
+                                   const float* S, const float* const* F, const sfseg_params* p,
+                                   int32_t kind, const double* x0, int32_t max_iters, double tol,
+                                   double* eigenvector, double* eigenvalue, int32_t* iterations_used,
+                                   int32_t mem) {
+    return guarded([&] {
+        if (!c || !p || !x0) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (max_iters < 1) fail(SFSEG_ERR_PARAMETER, "max_iters must be at least 1");
+        AffProblem P;
+        aff_setup(c, P, T, H, W, C, S, F, p, kind, mem);
+        const size_t n = static_cast<size_t>(P.n);
+        double* x = P.alloc<double>(n);
+        double* y = P.alloc<double>(n);
+        double* sc = P.scal->as<double>();
+        ck(cudaMemcpyAsync(y, x0, n * sizeof(double),
+                           mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           c->stream),
+           "upload x0");
+        const int g = static_cast<int>(std::min<long long>((P.n + 255) / 256, c->num_sms * 16LL));
+        // x0 / ||x0|| (oracle.cpp:223-225)
+        aff_sum<0>(c, P, y, nullptr, nullptr, sc, true);
+        double h[2];
+        ck(cudaMemcpyAsync(h, sc, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "norm");
+        ck(cudaStreamSynchronize(c->stream), "norm");
+        if (h[0] == 0.0) fail(SFSEG_ERR_PARAMETER, "power iteration needs a nonzero start vector");
+        sfk::k_div_scale<<<g, 256, 0, c->stream>>>(y, sc, x, P.n);
+        launched(c->stream, "k_div_scale");
+        int used = 0;
+        for (int k = 1; k <= max_iters; ++k) {  // oracle.cpp:229-243
+            aff_matvec(c, P, x, y);
+            aff_sum<0>(c, P, y, nullptr, nullptr, sc, true);             // ||y||
+            aff_sum<2>(c, P, y, x, sc, sc + 1, true);                    // ||y/||y|| - x||
+            ck(cudaMemcpyAsync(h, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "scalars");
+            ck(cudaStreamSynchronize(c->stream), "power iteration");
+            if (h[0] == 0.0) fail(SFSEG_ERR_DEGENERATE, "power iteration mapped the iterate to zero");
+            sfk::k_div_scale<<<g, 256, 0, c->stream>>>(y, sc, x, P.n);
+            launched(c->stream, "k_div_scale");
+            used = k;
+            if (h[1] < tol) break;
+        }
+        // eigenvalue = cluster_score(m, x) = x^T M x / x^T x (oracle.cpp:249-258)
+        aff_matvec(c, P, x, y);
+        aff_sum<0>(c, P, x, nullptr, nullptr, sc, false);
+        aff_sum<1>(c, P, x, y, nullptr, sc + 1, false);
+        ck(cudaMemcpyAsync(h, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "scalars");
+        if (eigenvector)
+            ck(cudaMemcpyAsync(eigenvector, x, n * sizeof(double),
+                               mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                               c->stream),
+               "eigenvector");
+        ck(cudaStreamSynchronize(c->stream), "power iteration");
+        if (eigenvalue) *eigenvalue = h[1] / h[0];
+        if (iterations_used) *iterations_used = used;
+    });
 }
 
 uint64_t sfseg_separable_convolution_count(void) {

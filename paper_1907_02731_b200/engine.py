@@ -43,7 +43,8 @@ __all__ = [
     "sfseg_step_channel", "normalize_l2", "project_binary", "threshold_final", "run",
     "separable_convolution_count", "Context", "default_context", "Error", "ParameterError",
     "ShapeError", "ValidationError", "DegenerateSolutionError", "CapacityError", "IoError",
-    "FormatError", "CorruptionError", "run_files", "volume_shape",
+    "FormatError", "CorruptionError", "run_files", "volume_shape", "affinity_matvec",
+    "power_iteration",
 ]
 
 ARITH_EXACT = N.SFSEG_ARITH_EXACT
@@ -575,3 +576,60 @@ def run_files(unary_path, pairwise_paths: Sequence, cfg: SfsegConfig, x0_path=No
                                    soft.ctypes.data_as(C.c_void_p), mask.ctypes.data_as(C.c_void_p),
                                    N.SFSEG_MEM_HOST))
     return RunResult(soft, mask, trace)
+
+
+_AFFINITY_KINDS = {"exact": N.SFSEG_AFFINITY_EXACT, "taylor": N.SFSEG_AFFINITY_TAYLOR,
+                   "taylor_channel_sum": N.SFSEG_AFFINITY_TAYLOR_CHANNEL_SUM}
+
+
+def _affinity_operands(features: FeatureSet, cfg: SfsegConfig, kind: str):
+    if kind not in _AFFINITY_KINDS:
+        raise ParameterError("kind must be 'exact', 'taylor' or 'taylor_channel_sum'")
+    S = np.ascontiguousarray(features.unary, np.float32)
+    if len(features.pairwise) == 0:
+        raise ValidationError("feature set needs at least one pairwise channel")
+    F = [np.ascontiguousarray(f, np.float32) for f in features.pairwise]
+    for f in F:
+        if f.shape != S.shape:
+            raise ShapeError("pairwise channel shape differs from unary shape")
+    ptrs = (C.c_void_p * len(F))(*[f.ctypes.data for f in F])
+    return S, F, ptrs, cfg.to_params(), _AFFINITY_KINDS[kind]
+
+
+def affinity_matvec(features: FeatureSet, cfg: SfsegConfig, x, kind: str = "taylor",
+                    ctx: Optional[Context] = None) -> np.ndarray:
+    """y = M x for the reference's explicit affinity (oracle.hpp:76-107,
+    oracle.cpp:191-207), matrix-free in fp64 on the GPU and without the
+    1e6-node cap (sfseg_affinity_matvec)."""
+    ctx = ctx or default_context()
+    S, F, ptrs, p, k = _affinity_operands(features, cfg, kind)
+    x = np.ascontiguousarray(x, np.float64)
+    if x.shape != S.shape:
+        raise ShapeError("matvec operand length mismatch")
+    y = np.empty_like(x)
+    T, H, W = S.shape
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_affinity_matvec(ctx.handle, T, H, W, len(F), S.ctypes.data,
+                                               C.cast(ptrs, C.c_void_p), C.byref(p), k,
+                                               x.ctypes.data, y.ctypes.data, N.SFSEG_MEM_HOST))
+    return y
+
+
+def power_iteration(features: FeatureSet, cfg: SfsegConfig, x0, max_iters: int, tol: float,
+                    kind: str = "taylor", ctx: Optional[Context] = None):
+    """The reference's power_iteration + cluster_score (oracle.cpp:219-258)
+    on the GPU: returns (eigenvector, eigenvalue, iterations_used)."""
+    ctx = ctx or default_context()
+    S, F, ptrs, p, k = _affinity_operands(features, cfg, kind)
+    x0 = np.ascontiguousarray(x0, np.float64)
+    if x0.shape != S.shape:
+        raise ShapeError("x0 length does not match matrix size")
+    vec = np.empty_like(x0)
+    val, used = C.c_double(), C.c_int32()
+    T, H, W = S.shape
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_affinity_power_iteration(
+            ctx.handle, T, H, W, len(F), S.ctypes.data, C.cast(ptrs, C.c_void_p), C.byref(p), k,
+            x0.ctypes.data, int(max_iters), float(tol), vec.ctypes.data, C.byref(val),
+            C.byref(used), N.SFSEG_MEM_HOST))
+    return vec, val.value, used.value

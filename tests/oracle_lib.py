@@ -219,6 +219,37 @@ class Reference(_Base):
         rc = self.lib.sfref_load_volume(str(path).encode(), dims, None, C.c_size_t(0))
         return rc, (tuple(int(d) for d in dims) if rc == 0 else None)
 
+    _KINDS = {"exact": 0, "taylor": 1, "taylor_channel_sum": 2}
+
+    def affinity_matvec(self, S, F, cfg, x, kind="taylor"):
+        """sfseg_ref::matvec(build_affinity_<kind>(...), x) (oracle.cpp:67-207);
+        returns (status, y)"""
+        S = np.ascontiguousarray(S, _F)
+        F = [np.ascontiguousarray(f, _F) for f in F]
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        T, H, W = S.shape
+        p = params(cfg)
+        rc = self.lib.sfref_affinity_matvec(C.c_uint32(T), C.c_uint32(H), C.c_uint32(W),
+                                            C.c_int32(len(F)), _vp(S), C.cast(_chans(F), C.c_void_p),
+                                            C.byref(p), C.c_int32(self._KINDS[kind]), _vp(x), _vp(y))
+        return rc, y
+
+    def power_iteration(self, S, F, cfg, x0, max_iters, tol, kind="taylor"):
+        """sfseg_ref::power_iteration (oracle.cpp:219-247): (vec, value, used)"""
+        S = np.ascontiguousarray(S, _F)
+        F = [np.ascontiguousarray(f, _F) for f in F]
+        x0 = np.ascontiguousarray(x0, np.float64)
+        vec = np.empty_like(x0)
+        val, used = C.c_double(), C.c_int32()
+        T, H, W = S.shape
+        p = params(cfg)
+        self._chk(self.lib.sfref_power_iteration(
+            C.c_uint32(T), C.c_uint32(H), C.c_uint32(W), C.c_int32(len(F)), _vp(S),
+            C.cast(_chans(F), C.c_void_p), C.byref(p), C.c_int32(self._KINDS[kind]), _vp(x0),
+            C.c_int32(max_iters), C.c_double(tol), _vp(vec), C.byref(val), C.byref(used)))
+        return vec, val.value, used.value
+
     def global_loop(self, S, F, cfg, iterations, threads=1):
         S = np.ascontiguousarray(S, _F)
         F = [np.ascontiguousarray(f, _F) for f in F]
