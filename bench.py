@@ -257,24 +257,32 @@ def main():
                                C.cast(fptrs, C.c_void_p), None, N.SFSEG_MEM_HOST))
 
         def timed_solves(arith, sampler=None):
+            """K solves timed on the library stream (CUDA events at the solve
+            boundaries, no per-launch events: those would sit between the
+            kernels of the programmatic-dependent-launch chain); then two
+            solves with per-launch events for the fused kernel's average."""
             c2 = E.SfsegConfig(**{**cfg.__dict__, "arith": arith})
             p = c2.to_params()
             for _ in range(args.warmup):
                 N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-            ctx.set_timing(True)
             ctx.synchronize()
             barrier()
-            solve_ms, kern_ms, launches = [], 0.0, 0
+            solve_ms = []
             import contextlib
             with (sampler or contextlib.nullcontext()):
                 for _ in range(args.steps):
                     N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
-                    tm = ctx.timing()
-                    solve_ms.append(tm.solve_ms)
-                    kern_ms += tm.step_kernel_ms
-                    launches += tm.step_launches
+                    solve_ms.append(ctx.timing().solve_ms)
             ctx.synchronize()
             barrier()
+            ctx.set_timing(True)
+            kern_ms, launches = 0.0, 0
+            for _ in range(2):
+                N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, iters, None))
+                tm = ctx.timing()
+                kern_ms += tm.step_kernel_ms
+                launches += tm.step_launches
+            ctx.synchronize()
             ctx.set_timing(False)
             return sum(solve_ms), kern_ms / max(1, launches)
 

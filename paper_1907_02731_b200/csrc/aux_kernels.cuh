@@ -242,6 +242,7 @@ __global__ void k_finalize(const double* part, int per_frame, double* frame_sum,
                            int mode_next, double lambda, double threshold_frac) {
     __shared__ double s[kAuxThreads];
     __shared__ bool is_last;
+    griddep_wait();  // PDL: the step's partials are complete
     const int t = blockIdx.x;
     const double* p = part + static_cast<size_t>(t) * per_frame;
     double acc = 0.0;

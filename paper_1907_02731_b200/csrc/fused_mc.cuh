@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
+    griddep_wait();  // PDL: the previous step / finalize has completed
     if (a.st->degenerate && SFK_MC_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
     __shared__ float red_max[SFK_RS_WIDE && SFK_RS_WREDUCE ? TY_ / BR_ : 1];
 
     const int tid = threadIdx.x;
+    griddep_wait();  // PDL: the previous step / finalize has completed
     if (a.st->degenerate && SFK_RS_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;

@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(FusedGeom<RT, R, CG, TY, TX, QY, STAGES>::NT, 
     __shared__ int prod_count;
 
     const int tid = threadIdx.x;
+    griddep_wait();  // PDL: the previous step / finalize has completed
     if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
 
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(32 * NWA + 256, 1) fused_step_ws(const __grid_
     __shared__ int prod_count;
 
     const int tid = threadIdx.x;
+    griddep_wait();  // PDL: the previous step / finalize has completed
     if (a.st->degenerate && SFK_EXP == 0) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;

@@ -404,6 +404,34 @@ const McVariant* pick_mc(int rt, int ry, int rx) {
     return best;
 }
 
+// Programmatic dependent launch for the per-iteration chain step -> finalize
+// -> step: the next kernel is scheduled while the previous one drains and
+// waits in griddep_wait() (every fused kernel and k_finalize call it before
+// touching the predecessor's results). SFSEG_PDL=0 turns it off.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SFSEG_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t stream,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 }  // namespace
@@ -809,7 +837,7 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
             cudaEventCreate(&e1);
             cudaEventRecord(e0, c->stream);
         }
-        v.kernel[kind]<<<grid_n, v.threads, v.smem[kind], c->stream>>>(a);
+        launch_pdl(v.kernel[kind], grid_n, v.threads, v.smem[kind], c->stream, a);
         launched(c->stream, "fused_step_mc launch");
         if (c->timing) {
             cudaEventRecord(e1, c->stream);
@@ -887,7 +915,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                 cudaEventCreate(&e1);
                 cudaEventRecord(e0, c->stream);
             }
-            (g == 0 ? v->kernel : v->kernel_acc)<<<grid_n, v->threads, v->smem, c->stream>>>(a);
+            launch_pdl(g == 0 ? v->kernel : v->kernel_acc, grid_n, v->threads, v->smem, c->stream, a);
             launched(c->stream, "fused_step launch");
             if (c->timing) {
                 cudaEventRecord(e1, c->stream);
@@ -942,9 +970,9 @@ void frame_sums(sfseg_ctx* c) {
 
 void finalize(sfseg_ctx* c, IterState* st, double* norms, int iter_index, int mode_next,
               double lambda, double frac) {
-    sfk::k_finalize<<<c->Tout(), sfk::kAuxThreads, 0, c->stream>>>(
-        c->part, c->nbands() * c->nhalves(), c->frame_sum, c->frame_max, c->ticket, st, norms,
-        iter_index, mode_next, lambda, frac);
+    launch_pdl(sfk::k_finalize, c->Tout(), sfk::kAuxThreads, 0, c->stream, c->part,
+               c->nbands() * c->nhalves(), c->frame_sum, c->frame_max, c->ticket, st, norms,
+               iter_index, mode_next, lambda, frac);
     launched(c->stream, "k_finalize");
 }
 
@@ -1011,7 +1039,9 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
         const int mode_next = it >= p->binarize_start ? 2 : 1;
         finalize(c, c->st, c->norms, it - first, mode_next, lambda_for(p, it), p->threshold_frac);
         c->cur = dst;
-        ck(cudaEventRecord(iter_ev[it - first + 1], c->stream), "event");
+        // per-iteration events only when per-iteration times are wanted: an
+        // event between two kernels stops the programmatic (PDL) overlap
+        if (rec || c->timing || it == last) ck(cudaEventRecord(iter_ev[it - first + 1], c->stream), "event");
     }
     std::vector<double> norms(n);
     ck(cudaMemcpyAsync(norms.data(), c->norms, n * sizeof(double), cudaMemcpyDeviceToHost,
