@@ -111,6 +111,14 @@
 #ifndef SFK_RS_CPA
 #define SFK_RS_CPA 0
 #endif
+// SFK_RS_HALF=1: the x-pass rows beyond the first 8 NWA (the 2R halo rows
+// below the tile) run as 4-wide strips spread over the first warps, so no
+// A warp does two full 8-row passes per plane. Measured 207.4 us against
+// 205.9 (warp 0's x-pass drops 2396 -> 2126 cycles per plane, the plane
+// period does not move), so off.
+#ifndef SFK_RS_HALF
+#define SFK_RS_HALF 0
+#endif
 
 namespace sfk {
 
@@ -308,6 +316,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
         };
         constexpr int PROD = SFK_RS_PRODUCER;
         constexpr bool PSPLIT = SFK_RS_PSPLIT != 0;
+        constexpr bool HALF = SFK_RS_HALF != 0 && 8 * NWA <= BH && (BH - 8 * NWA) * (TX / 4) <= NA;
         // PSPLIT: box `pbox` of every plane is issued by lane 0 of warp
         // NWA - 3 + pbox, each with its own copy of the plane cursor
         const int pbox = (tid >> 5) - (NWA - 3);
@@ -352,21 +361,24 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
         // one x-pass item (conv3d.cpp:88-101): row r, strip sx (SW outputs).
         // u runs as column pairs (2k, 2k+1) with tap pairs (w[e], w[e-1]);
         // (F u, F^2 u) runs as a pair per column with a broadcast tap.
-        auto item = [&](auto sig_c, const float* rs, float* xbu, float* xbp, int r, int sx) {
+        // SWI: strip width (8; 4 for the HALF second pass)
+        auto item = [&](auto sig_c, auto sw_c, const float* rs, float* xbu, float* xbp, int r, int sx) {
             constexpr bool SIG = decltype(sig_c)::value;
-            const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + 2 * sx;
+            constexpr int SW = decltype(sw_c)::value;
+            constexpr int NINXI = SW + 2 * R, NLDI = (G::XOFF + NINXI + 3) / 4;
+            const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + sx * (SW / 4);
             float2 ou[SW / 2];
             float2 op[SW];
             float4 yv, sv, fv;
 #pragma unroll
-            for (int m4 = 0; m4 < G::NLD * 4; ++m4) {
+            for (int m4 = 0; m4 < NLDI * 4; ++m4) {
                 if (m4 % 4 == 0) {
                     yv = py[m4 / 4];
                     sv = py[FB / 4 + m4 / 4];
                     fv = py[2 * (FB / 4) + m4 / 4];
                 }
                 const int m = m4 - G::XOFF;
-                if (m < 0 || m >= G::NINX) continue;
+                if (m < 0 || m >= NINXI) continue;
                 const int c = m4 % 4;
                 const float y = c == 0 ? yv.x : c == 1 ? yv.y : c == 2 ? yv.z : yv.w;
                 const float s = c == 0 ? sv.x : c == 1 ? sv.y : c == 2 ? sv.z : sv.w;
@@ -425,6 +437,23 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
             const float* rs = raw + static_cast<size_t>(s) * 3 * FB;
             float* xbu = xb + b * XBUF;
             float* xbp = xbu + XBU;
+            using W8 = std::integral_constant<int, 8>;
+            using W4 = std::integral_constant<int, 4>;
+            if constexpr (HALF) {
+                // pass 1: box rows 8 xw .. 8 xw + 7, four 8-wide strips; pass 2:
+                // the last BH - 8 NWA rows as 4-wide strips over the first warps
+                if (!(SFK_RS_EXP & 1)) {
+                    const int r = xw * 8 + (xl & 7);
+                    if (sigm) item(std::true_type{}, W8{}, rs, xbu, xbp, r, xl >> 3);
+                    else item(std::false_type{}, W8{}, rs, xbu, xbp, r, xl >> 3);
+                    const int it2 = xw * 32 + xl;
+                    if (it2 < (BH - 8 * NWA) * (TX / 4)) {
+                        const int r2 = 8 * NWA + it2 / (TX / 4), s2 = it2 % (TX / 4);
+                        if (sigm) item(std::true_type{}, W4{}, rs, xbu, xbp, r2, s2);
+                        else item(std::false_type{}, W4{}, rs, xbu, xbp, r2, s2);
+                    }
+                }
+            } else {
 #pragma unroll
             for (int k = 0; k < G::XPASS; ++k) {
                 const int blk = xw + k * NWA;
@@ -432,9 +461,10 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                 const int r = blk * 8 + (xl & 7);
                 if (r >= BH || (SFK_RS_EXP & 1)) continue;
                 if (sigm && !(SFK_RS_EXP & 4))
-                    item(std::true_type{}, rs, xbu, xbp, r, xl >> 3);
+                    item(std::true_type{}, W8{}, rs, xbu, xbp, r, xl >> 3);
                 else
-                    item(std::false_type{}, rs, xbu, xbp, r, xl >> 3);
+                    item(std::false_type{}, W8{}, rs, xbu, xbp, r, xl >> 3);
+            }
             }
             if (tid == 0 || tid == 64) SFK_T(cnt, tid ? 14 : 3);
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores

@@ -15,13 +15,20 @@ from paper_1907_02731_b200.sharding import CudaBackend, buffer_range, shard_rang
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,arith,binarize", [(2, "exact", False), (3, "fast", True)])
-def test_shards_match_single_context(world, arith, binarize):
-    prob = synth.config(1, frames=12)[0]
+@pytest.mark.parametrize("world,arith,binarize,idx", [
+    (2, "exact", False, 1), (3, "fast", True, 1),
+    (2, "fast", False, 2),  # C = 8: the (C + 2)-field launches (fused_mc.cuh) per shard
+    (3, "fast", True, 4),   # C = 3, radii (4, 10, 10)
+])
+def test_shards_match_single_context(world, arith, binarize, idx):
+    prob = synth.config(idx, frames=12)[0]
     fs, _ = prob.generate()
+    if idx != 1:  # crop H, W so the test stays small
+        fs = E.FeatureSet(np.ascontiguousarray(fs.unary[:, :100, :150]),
+                          [np.ascontiguousarray(f[:, :100, :150]) for f in fs.pairwise])
     cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, "iterations": 6,
                            "binarize_start": 3 if binarize else 7})
-    T, H, W = prob.shape
+    T, H, W = fs.unary.shape
     halo = cfg.kernel.radii[0]
     ranks = []
     for r in range(world):
