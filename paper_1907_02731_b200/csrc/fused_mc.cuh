@@ -29,7 +29,19 @@
 // last launch, the canonical reductions. Every field is one "single" slot:
 // two neighbouring outputs take one input with one FFMA2 and a tap pair
 // (w[e], w[e-1]) — columns in the x-pass, rows in the y-pass.
+//
+// KIND 2 (EXACT, one launch per channel, the reference's own 1 + 2C form):
+// boxes x, S^p, f; fields u, f u, (f f) u evaluated left to right
+// (engine.cpp:92-100); every product and sum separately rounded in the
+// reference's tap order (conv3d.cpp:88-165: paired FFMA2 with runtime
+// zero / one operands, so no contraction), the normalisation and sigmoid
+// applied on load in fp64 (engine.cpp:178, 196-203), the recombination and
+// channel sum of engine.cpp:113-119, 157-162, and fp64 canonical reductions.
+// A step is bit-identical to the reference's sfseg_step at the radii the
+// warp-specialised EXACT kernel (fused_ws.cuh) has no room for (c2, c4).
 #pragma once
+
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "fused_step.cuh"  // PlaneStream, Arith, ffma2
@@ -57,8 +69,11 @@
 
 namespace sfk {
 
-template <int RT, int R, int NF, bool HEAD>
+enum McKind { MC_HEAD = 0, MC_TAIL = 1, MC_EXACT = 2 };
+
+template <int RT, int R, int NF, int KIND>
 struct McGeom {
+    static constexpr bool HEAD = KIND == MC_HEAD, EXACT = KIND == MC_EXACT;
     static constexpr int TY = 64, TX = 32, BR = 8, NWA = SFK_MC_NWA, NWB = TY / BR, STAGES = SFK_MC_STAGES;
     static constexpr int NA = 32 * NWA, NB = 32 * NWB, NT = NA + NB;
     static constexpr int K = 2 * RT + 1;
@@ -68,7 +83,8 @@ struct McGeom {
     static constexpr int BW = TX + HX + HR, BW4 = BW / 4;
     static constexpr int XOFF = HX - R;
     static constexpr int FB = (BH * BW + 31) / 32 * 32;
-    static constexpr int NR = NF + 1;  // raw boxes: HEAD x, S^p, Q; TAIL U, f_a [, f_b]
+    // raw boxes: HEAD x, S^p, Q; TAIL U, f_a [, f_b]; EXACT x, S^p, f
+    static constexpr int NR = EXACT ? 3 : NF + 1;
     static constexpr int SW = 8;
     static constexpr int NINX = SW + 2 * R;
     static constexpr int NLD = (XOFF + NINX + 3) / 4;
@@ -79,7 +95,8 @@ struct McGeom {
     static constexpr int NXB = SFK_MC_NXB;
     // recombination operands (TMA slabs, one emitted plane ahead): S^p, Q |
     // S^p, f_a [, f_b], y of the earlier launches
-    static constexpr int NOP = HEAD ? 2 : NF + 2;
+    // (EXACT: S^p, f, y of the earlier channels)
+    static constexpr int NOP = HEAD ? 2 : EXACT ? 3 : NF + 2;
     static constexpr int SLAB = BR * TX;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NR * FB;
     static constexpr size_t XB_FLOATS = size_t(NXB) * NF * XBU;
@@ -102,16 +119,17 @@ struct McGeom {
     static_assert((TXU / 4) % 2 == 1, "conflict-free x-pass rows");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
     static_assert(K * RW <= TCOLS / 2, "TMEM ring of one thread");
-    static_assert(NF >= 1 && NF <= 2 && (NF == 2 || !HEAD), "field groups");
+    static_assert(EXACT ? NF == 3 : (NF >= 1 && NF <= 2 && (NF == 2 || !HEAD)), "field groups");
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
     static_assert(NWA % 4 == 0 && NWB % 4 == 0, "setmaxnreg acts on whole warpgroups");
 };
 
-template <int RT, int R, int NF, bool HEAD>
-__global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
+template <int RT, int R, int NF, int KIND>
+__global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
     fused_step_mc(const __grid_constant__ FusedArgs a) {
-    using G = McGeom<RT, R, NF, HEAD>;
-    using A = Arith<true>;
+    using G = McGeom<RT, R, NF, KIND>;
+    constexpr bool HEAD = G::HEAD, EXACT = G::EXACT;
+    using A = Arith<!EXACT>;
     constexpr int BR = G::BR, TY = G::TY, TX = G::TX, NA = G::NA, NB = G::NB, K = G::K, NWB = G::NWB;
     constexpr int BH = G::BH, BW = G::BW, FB = G::FB, BW4 = G::BW4, SW = G::SW, NR = G::NR;
     constexpr int TXU = G::TXU, XBU = G::XBU, SLAB = G::SLAB, NXB = G::NXB, STAGES = G::STAGES;
@@ -155,6 +173,17 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
     }
     __syncthreads();
     const float2 zero2 = make_float2(0.0f, 0.0f);
+    // EXACT: p = w x + 0 and acc = acc * 1 + p with run-time 0 / 1, so every
+    // product and every sum is rounded on its own (no FMA contraction)
+    const float2 zr2 = make_float2(a.zero, a.zero), one2 = make_float2(a.one, a.one);
+    auto acc2 = [&](float2 acc, float2 x, float2 w, bool first) {
+        if constexpr (EXACT) {
+            const float2 pr = ffma2(x, w, zr2);
+            return first ? pr : ffma2(acc, one2, pr);
+        } else {
+            return ffma2(x, w, first ? zero2 : acc);
+        }
+    };
 
     if (tid < NA) {
         // =====================================================================
@@ -182,8 +211,8 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
             uint64_t* bar = &raw_full[s];
             const int bx = pq.tile_x * TX - G::HX, by = pq.tile_y * TY - R, bt = tg - a.buf_t0;
             if (pbox == 0) mbar_arrive_expect_tx(bar, NR * BH * BW * sizeof(float));
-            const CUtensorMap* map = pbox == 0 ? &a.tm_x : HEAD ? (pbox == 1 ? &a.tm_sp : &a.tm_f[0])
-                                                               : &a.tm_f[pbox - 1];
+            const CUtensorMap* map = pbox == 0 ? &a.tm_x : (HEAD || EXACT) ? (pbox == 1 ? &a.tm_sp : &a.tm_f[0])
+                                                                        : &a.tm_f[pbox - 1];
             tma_load_3d(dst, map, bar, bx, by, bt);
             ++pcount;
             pq.next();
@@ -192,12 +221,13 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
             pq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
             for (int s = 0; s < STAGES; ++s) issue_box();
         }
-        const bool sigm = HEAD && st.mode == 2;
+        const bool sigm = (HEAD || EXACT) && st.mode == 2;
+        const bool norm = EXACT && st.mode == 1;  // EXACT normalises on load
         const int xw = tid >> 5, xl = tid & 31;  // lane -> (row xl & 7, strip xl >> 3)
 
         // one x-pass item: box row r, strip sx (SW outputs as column pairs)
         auto item = [&](auto sig_c, const float* rs, float* xbb, int r, int sx, float* urow) {
-            constexpr bool SIG = decltype(sig_c)::value;
+            constexpr bool SIG = decltype(sig_c)::value == 2, NRM = decltype(sig_c)::value == 1;
             const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + 2 * sx;
             float2 ou[NF][SW / 2];
             float uc[SW];  // HEAD: u at this strip's own points (for U)
@@ -215,7 +245,14 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
 #pragma unroll
                 for (int i = 0; i < NR; ++i) e4[i] = c == 0 ? v[i].x : c == 1 ? v[i].y : c == 2 ? v[i].z : v[i].w;
                 float phi[NF];
-                if constexpr (HEAD) {
+                if constexpr (EXACT) {
+                    const float x = SIG ? A::load_sigmoid(e4[0], st)
+                                        : NRM ? A::load_norm(e4[0], st.inv, st.inv_f) : e4[0];
+                    const float u = xmul(e4[1], x);  // engine.cpp:92-98, left to right
+                    phi[0] = u;
+                    phi[1] = xmul(e4[2], u);
+                    phi[2] = xmul(xmul(e4[2], e4[2]), u);
+                } else if constexpr (HEAD) {
                     const float x = SIG ? A::load_sigmoid(e4[0], st) : e4[0];
                     const float u = e4[1] * x;  // engine.cpp:92-100
                     phi[0] = u;
@@ -231,7 +268,8 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                     for (int k = 0; k < SW / 2; ++k) {
                         const int e = m - 2 * k;
                         if (e < 0 || e > 2 * R + 1) continue;
-                        ou[i][k] = ffma2(make_float2(phi[i], phi[i]), a.tpair_x[e], e == 0 ? zero2 : ou[i][k]);
+                        // x-pass starts from acc = 0 (conv3d.cpp:92): 0 + p = p
+                        ou[i][k] = acc2(ou[i][k], make_float2(phi[i], phi[i]), a.tpair_x[e], e == 0);
                     }
                 }
             }
@@ -276,10 +314,15 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                         urow = a.u_out + (static_cast<size_t>(tg - a.buf_t0) * a.H + oy) * a.pitch +
                                q.tile_x * TX;
                 }
+                using L0 = std::integral_constant<int, 0>;
+                using L1 = std::integral_constant<int, 1>;
+                using L2 = std::integral_constant<int, 2>;
                 if (sigm)
-                    item(std::true_type{}, rs, xbb, r, xl >> 3, urow);
+                    item(L2{}, rs, xbb, r, xl >> 3, urow);
+                else if (EXACT && norm)
+                    item(L1{}, rs, xbb, r, xl >> 3, urow);
                 else
-                    item(std::false_type{}, rs, xbb, r, xl >> 3, urow);
+                    item(L0{}, rs, xbb, r, xl >> 3, urow);
             }
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
@@ -298,7 +341,9 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
         const int lane = bt & 31;
         const int wb = bt >> 5;
         const bool last = a.last_group;
-        const float scale = st.mode == 1 ? st.inv_f : 1.0f;  // deferred 1/||y_k|| (FAST)
+        // deferred 1/||y_k|| (FAST; EXACT normalised on load)
+        const float scale = (!EXACT && st.mode == 1) ? st.inv_f : 1.0f;
+        const bool first = a.first_group;  // EXACT: no earlier channel to add
         constexpr int TCOLS = G::TCOLS;
         if (wb == 0) tmem_alloc<TCOLS>(&tmem_base_sh);
         tcgen05_fence_before();
@@ -313,13 +358,15 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
         PlaneStream& eq = slabq[wb];  // lane 0 only
         auto issue_slab = [&]() {
             if (eq.done) return;
-            mbar_arrive_expect_tx(sfull, NOP * SLAB * sizeof(float));
+            const bool yprev = !HEAD && !(EXACT && first);
+            mbar_arrive_expect_tx(sfull, (yprev ? NOP : NOP - (HEAD ? 0 : 1)) * SLAB * sizeof(float));
             const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
             tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
 #pragma unroll
-            for (int i = 0; i < (HEAD ? 1 : NF); ++i) tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
-            if constexpr (!HEAD)  // y so far: written by the previous launch (stream order)
-                tma_load_3d(slab + (NOP - 1) * SLAB, &a.tm_out, sfull, x, y, t - a.buf_t0 + a.out_buf_t0);
+            for (int i = 0; i < ((HEAD || EXACT) ? 1 : NF); ++i)
+                tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
+            if (yprev)  // y so far: written by the previous launch (stream order)
+                tma_load_3d(slab + (NOP - 1) * SLAB, &a.tm_out, sfull, x, y, t + a.buf_t0 - a.out_buf_t0);
             eq.next();
         };
         if (lane == 0) {
@@ -350,8 +397,8 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                     for (int e = 0; e <= 2 * R + 1; ++e) {
 #pragma unroll
                         for (int k = 0; k < BR / 2; ++k)
-                            cur[i][k] = ffma2(make_float2(vin[2 * k + e], vin[2 * k + e]), a.tpair_y[e],
-                                              e == 0 ? zero2 : cur[i][k]);
+                            cur[i][k] = acc2(cur[i][k], make_float2(vin[2 * k + e], vin[2 * k + e]),
+                                             a.tpair_y[e], e == 0);
                     }
                 }
                 if (SFK_MC_EXP & 2)
@@ -395,7 +442,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                                 const float2 lu = (d == K - 1 || (SFK_MC_EXP & 4))
                                                       ? cur[i][k]
                                                       : make_float2(w[j][i][2 * k], w[j][i][2 * k + 1]);
-                                tacc[i][k] = ffma2(lu, w2, d == 0 ? zero2 : tacc[i][k]);
+                                tacc[i][k] = acc2(tacc[i][k], lu, w2, d == 0);
                             }
                     }
                 }
@@ -421,7 +468,11 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                     float g[NF];
 #pragma unroll
                     for (int i = 0; i < NF; ++i) g[i] = (r & 1) ? tacc[i][r / 2].y : tacc[i][r / 2].x;
-                    if constexpr (HEAD) {
+                    if constexpr (EXACT) {
+                        // engine.cpp:113-119 (u, F u, F^2 u convolved), channel sum :157-162
+                        const float term = A::recombine(opv[0][r], opv[1][r], a.inv_alpha, g[0], g[2], g[1]);
+                        v[r] = first ? term : xadd(opv[2][r], term);
+                    } else if constexpr (HEAD) {
                         // S^p ((C/alpha - Q) G(u) - G(Q u))
                         v[r] = (opv[0][r] * scale) * ((a.c_inv_alpha - opv[1][r]) * g[0] - g[1]);
                     } else {
@@ -431,7 +482,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                         v[r] = (2.0f * opv[0][r] * scale) * sfg;
                     }
                 }
-                if constexpr (!HEAD) {  // y of the earlier launches (zero-filled past the edge)
+                if constexpr (KIND == MC_TAIL) {  // y of the earlier launches (zero-filled past the edge)
 #pragma unroll
                     for (int r = 0; r < BR; ++r) v[r] += opv[NOP - 1][r];
                 }
@@ -453,9 +504,12 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, HEAD>::NT, 1)
                     // column sums, xor-butterfly over the 32 columns
 #pragma unroll
                     for (int h = 0; h < BR / 4; ++h) {
-                        float cs = 0.0f;
+                        // EXACT: fp64 column sums and butterfly (fused_ws.cuh)
+                        using RT_ = std::conditional_t<EXACT, double, float>;
+                        RT_ cs = 0;
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) cs = fmaf(v[4 * h + r], v[4 * h + r], cs);
+                        for (int r = 0; r < 4; ++r)
+                            cs += static_cast<RT_>(v[4 * h + r]) * static_cast<RT_>(v[4 * h + r]);
 #pragma unroll
                         for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
                         const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + h;

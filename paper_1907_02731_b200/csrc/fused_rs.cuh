@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                         d_tx = q.tile_x;
                         d_ty = q.tile_y;
                         dpend = true;
-                    } else {
+                    } else if (!(SFK_RS_EXP & 32)) {
                         reduce_plane(v, to, q.tile_x, q.tile_y);
                     }
                 }

@@ -283,8 +283,8 @@ FusedVariant variant_rs() {
 struct McVariant {
     int rt, r;
     int threads, box_w, box_h;
-    size_t smem[3];          // head, tail of 2 channels, tail of 1
-    void (*kernel[3])(FusedArgs);
+    size_t smem[4];          // head, tail of 2 channels, tail of 1, EXACT per channel
+    void (*kernel[4])(FusedArgs);
 };
 
 template <int RT, int R>
@@ -292,18 +292,21 @@ McVariant variant_mc() {
     McVariant v;
     v.rt = RT;
     v.r = R;
-    using GH = sfk::McGeom<RT, R, 2, true>;
-    using G2 = sfk::McGeom<RT, R, 2, false>;
-    using G1 = sfk::McGeom<RT, R, 1, false>;
+    using GH = sfk::McGeom<RT, R, 2, sfk::MC_HEAD>;
+    using G2 = sfk::McGeom<RT, R, 2, sfk::MC_TAIL>;
+    using G1 = sfk::McGeom<RT, R, 1, sfk::MC_TAIL>;
+    using GE = sfk::McGeom<RT, R, 3, sfk::MC_EXACT>;
     v.threads = GH::NT;
     v.box_w = GH::BW;
     v.box_h = GH::BH;
     v.smem[0] = GH::SMEM_BYTES;
     v.smem[1] = G2::SMEM_BYTES;
     v.smem[2] = G1::SMEM_BYTES;
-    v.kernel[0] = sfk::fused_step_mc<RT, R, 2, true>;
-    v.kernel[1] = sfk::fused_step_mc<RT, R, 2, false>;
-    v.kernel[2] = sfk::fused_step_mc<RT, R, 1, false>;
+    v.smem[3] = GE::SMEM_BYTES;
+    v.kernel[0] = sfk::fused_step_mc<RT, R, 2, sfk::MC_HEAD>;
+    v.kernel[1] = sfk::fused_step_mc<RT, R, 2, sfk::MC_TAIL>;
+    v.kernel[2] = sfk::fused_step_mc<RT, R, 1, sfk::MC_TAIL>;
+    v.kernel[3] = sfk::fused_step_mc<RT, R, 3, sfk::MC_EXACT>;
     return v;
 }
 
@@ -762,9 +765,9 @@ float* ensure_q(sfseg_ctx* c, const std::vector<float*>& Fch) {
 // channels accumulating into y; the last launch emits the reductions
 void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
                     const IterState* st, float* out, const std::vector<float*>& Fch,
-                    const McVariant& v) {
-    float* q = ensure_q(c, Fch);
-    float* u = tmp_vol(c, 0);
+                    const McVariant& v, bool exact = false) {
+    float* q = exact ? nullptr : ensure_q(c, Fch);
+    float* u = exact ? nullptr : tmp_vol(c, 0);
     FusedVariant fv;  // taps / tensor-map geometry
     fv.rt = v.rt;
     fv.r = v.r;
@@ -806,17 +809,22 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
     static bool attr_set[16] = {};
     const int vidx = static_cast<int>(&v - mc_variants().data());
     if (!attr_set[vidx]) {
-        for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 4; ++i)
             ck(cudaFuncSetAttribute(v.kernel[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(v.smem[i])),
                "cudaFuncSetAttribute");
         attr_set[vidx] = true;
     }
     const int C = static_cast<int>(Fch.size());
-    const int ntail = (C + 1) / 2;
+    const int ntail = exact ? C - 1 : (C + 1) / 2;
     for (int g = 0; g <= ntail; ++g) {
         int kind = 0;
-        if (g == 0) {
+        if (exact) {  // one launch per channel: boxes x, S^p, f_g; operands S^p, f_g, y
+            kind = 3;
+            a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, fv.tx, 8);
+        } else if (g == 0) {
             a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(q, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(q, c->T, c->H, c->W, c->P, fv.tx, 8);
@@ -858,6 +866,13 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
     const McVariant* mc = (fma && Fch.size() > 1) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
     if (mc) {
         launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc);
+        return;
+    }
+    // EXACT beyond the warp-specialised instantiations (c2, c4 radii): the
+    // per-channel EXACT launches of fused_mc.cuh
+    const McVariant* mce = (!fma && !v) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
+    if (mce) {
+        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mce, true);
         return;
     }
     if (v) {
