@@ -870,7 +870,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
     }
     // EXACT beyond the warp-specialised instantiations (c2, c4 radii): the
     // per-channel EXACT launches of fused_mc.cuh
-    const McVariant* mce = (!fma && !v) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
+    static const bool exact_mc = env_flag("SFSEG_EXACT_MC");  // prefer it over fused_ws too
+    const McVariant* mce = (!fma && (!v || exact_mc)) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
     if (mce) {
         launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mce, true);
         return;
