@@ -21,4 +21,13 @@ for a in fast exact; do
   timeout 400 ncu --set full --clock-control none --import-source on -k regex:fused_step_ -s 1 -c 1 \
     -o "$OUT/full_$a" python tools/prof_run.py --iters 3 --arith $a > "$OUT/ncu_full_$a.log" 2>&1 || echo "full capture $a failed"
 done
+# the .ncu-rep files are ~20 MB each and gpurun_out/ travels back only under
+# 64 MiB: export the raw pages (and the SASS source page of the FAST kernel)
+# here and drop the reports unless KEEP_REPS=1
+for a in fast exact; do
+  [ -f "$OUT/full_$a.ncu-rep" ] || continue
+  ncu -i "$OUT/full_$a.ncu-rep" --page raw --csv > "$OUT/full_$a.raw.csv" 2>/dev/null
+  [ "$a" = fast ] && ncu -i "$OUT/full_$a.ncu-rep" --page source --csv --print-source sass > "$OUT/full_$a.sass.csv" 2>/dev/null
+  [ "${KEEP_REPS:-0}" = 1 ] || rm -f "$OUT/full_$a.ncu-rep"
+done
 ls -la "$OUT"

@@ -70,10 +70,14 @@ KEYS = [
 ]
 for a in ("fast", "exact"):
     rep = SRC / f"full_{a}.ncu-rep"
-    if not rep.exists():
+    rawf = SRC / f"full_{a}.raw.csv"  # exported on the box (tools/profile_round.sh)
+    if rawf.exists():
+        raw = rawf.read_text()
+    elif rep.exists():
+        raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+    else:
         continue
-    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
