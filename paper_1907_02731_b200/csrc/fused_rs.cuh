@@ -119,6 +119,14 @@
 #ifndef SFK_RS_HALF
 #define SFK_RS_HALF 0
 #endif
+// SFK_RS_CPS: CTAs resident per SM (2 with a half-height tile: two
+// independent pipelines per SM hide each other's barrier waits); the
+// setmaxnreg budgets then share each SMSP's 512 registers per lane slot
+// Measured: TY = 32, 4 + 4 warps, 2 stages, 2 CTAs per SM: 254.7 us
+// against 206 (the 2R halo rows cost more than the second pipeline hides).
+#ifndef SFK_RS_CPS
+#define SFK_RS_CPS 1
+#endif
 
 namespace sfk {
 
@@ -198,7 +206,9 @@ struct RsGeom {
 #endif
     static constexpr int RA = SFK_RS_RA;
     static constexpr int NW = NWA + NWB + NWC;
-    static constexpr int RPOOL = (512 / ((NW + 3) / 4)) / 8 * 8;
+    static constexpr int CPS = SFK_RS_CPS;
+    static constexpr int SMSP_REGS = 512 / CPS;  // per lane slot, this CTA's share
+    static constexpr int RPOOL = (SMSP_REGS / ((NW + 3) / 4)) / 8 * 8;
     // unsplit: the B warps take what A gives back. SPLIT: B keeps the launch
     // grant and the C warps take what A gives back.
     static constexpr int rb_for(int s) {
@@ -209,10 +219,10 @@ struct RsGeom {
                 else if (SPLIT && w < NWA + NWB) ++wk;
                 else ++wb;
             }
-        return wb ? (512 - wa * RA - wk * RPOOL) / wb : 512;
+        return wb ? (SMSP_REGS - wa * RA - wk * RPOOL) / wb : SMSP_REGS;
     }
     static constexpr int rb_min() {
-        int m = 512;
+        int m = SMSP_REGS;
         for (int s = 0; s < 4; ++s) m = rb_for(s) < m ? rb_for(s) : m;
         return m;
     }
@@ -231,7 +241,7 @@ struct RsGeom {
 };
 
 template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool TMR_, bool ACC>
-__global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT, 1)
+__global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT, SFK_RS_CPS)
     fused_step_rs(const __grid_constant__ FusedArgs a) {
     using G = RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>;
     using A = Arith<true>;

@@ -194,6 +194,7 @@ struct FusedVariant {
     void (*kernel_acc)(FusedArgs);  // later channel groups (y += terms); may equal kernel
     int box_w, box_h;
     int slab_h = 8;  // rows of the recombination-operand / output TMA boxes
+    int ctas_per_sm = 1;  // persistent grid = ctas_per_sm x SMs
 };
 
 template <int RT, int R, int TY, int TX, bool FMA>
@@ -265,6 +266,7 @@ FusedVariant variant_rs() {
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
     v.slab_h = (SFK_RS_WIDE && !TMR) ? TY : 8;
+    v.ctas_per_sm = SFK_RS_CPS;
     v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
     v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, true>;
     v.box_w = G::BW;
@@ -276,7 +278,7 @@ FusedVariant variant_rs() {
 // t-pass ring in tensor memory (a 7- or 9-plane register ring does not fit)
 #define SFK_VARIANTS_RS()                                                                  \
     variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>(),       \
-        variant_rs<3, 7, 2, true>(), variant_rs<4, 10, 2, true>()
+        variant_rs<3, 7, 2, true, 8, 64, 8>(), variant_rs<4, 10, 2, true, 8, 64, 8>()
 
 // FAST, C > 1: (C + 2)-field launches (fused_mc.cuh): a HEAD (u, Q u) and
 // TAILs of one or two channels (f_a u [, f_b u])
@@ -906,7 +908,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         a.nbands = c->nbands();
         a.nhalves = c->nhalves();
         const int ntiles = a.tiles_x * a.tiles_y;
-        const int grid_n = c->num_sms;
+        const int grid_n = c->num_sms * v->ctas_per_sm;
         upload_schedule(c, ntiles, c->Tout(), grid_n);
         a.sched = c->sched_seg;
         a.sched_off = c->sched_off;
@@ -1290,6 +1292,7 @@ void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
     c->cur = -1;
     c->has_x0 = false;
     c->resident = false;  // stateless operators reuse the resident buffers
+    c->q_for.clear();     // the channel buffers get new contents: Q is stale
 }
 
 void reduce_volume(sfseg_ctx* c, float* v, IterState* st, int mode_next, double lambda,
@@ -2033,7 +2036,7 @@ int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C
         }
         c->resident = true;
         c->q_for.clear();  // channel contents changed
-    });
+        });
 }
 
 int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_shard_io* io) {

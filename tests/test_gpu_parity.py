@@ -174,13 +174,16 @@ MC_CASES = [
 
 @pytest.mark.parametrize("shape,radii,sigmas,C", MC_CASES)
 def test_step_multichannel_fast_within_tolerance(shape, radii, sigmas, C):
-    S, F = _features(shape, 21, channels=C)
-    x = random_volume(shape, 77)
-    cfg = _cfg(radii, sigmas, 1.0, 0.1, arith="fast")
-    fs = E.FeatureSet(S, F)
-    got = E.sfseg_step(x, fs, cfg).astype(np.float64)
-    want = Oracle().step(x, S, F, cfg).astype(np.float64)
-    assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
+    # twice with the same shape and new channel data: the per-solve derived
+    # fields (Q, 2 S^p f_c) must not survive a change of the channels
+    for seed in (21, 121):
+        S, F = _features(shape, seed, channels=C)
+        x = random_volume(shape, 77)
+        cfg = _cfg(radii, sigmas, 1.0, 0.1 if seed == 21 else 0.3, arith="fast")
+        fs = E.FeatureSet(S, F)
+        got = E.sfseg_step(x, fs, cfg).astype(np.float64)
+        want = Oracle().step(x, S, F, cfg).astype(np.float64)
+        assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
 
 
 def test_run_c1_cropped_fast_matches_reference():
