@@ -255,6 +255,33 @@ class ShardedSolver:
             parts.append(bufs[r][: b - a])
         return torch.cat(parts).contiguous()  # frame order
 
+    def _gather_sums(self, frame_sum, frame_max):
+        """Both per-frame vectors in ONE all-gather (frame max widened to fp64,
+        exactly): one collective per iteration instead of two. Returns
+        (sums fp64, max fp32) in frame order."""
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return frame_sum, frame_max
+        n, tm = frame_sum.numel(), self.tmax
+        packed = torch.zeros(2 * tm, dtype=torch.float64, device=frame_sum.device)
+        packed[:n] = frame_sum
+        packed[tm:tm + n] = frame_max.to(torch.float64)
+        try:
+            allp = torch.empty(self.world * 2 * tm, dtype=torch.float64, device=packed.device)
+            dist.all_gather_into_tensor(allp, packed, group=self.group)
+            bufs = list(allp.view(self.world, 2 * tm))
+        except (RuntimeError, AttributeError, NotImplementedError):  # backends without it
+            bufs = [torch.empty_like(packed) for _ in range(self.world)]
+            dist.all_gather(bufs, packed, group=self.group)
+        sums, maxs = [], []
+        for r in range(self.world):
+            a, b = shard_range(self.T, self.world, r)
+            sums.append(bufs[r][: b - a])
+            maxs.append(bufs[r][tm: tm + b - a])
+        return torch.cat(sums).contiguous(), torch.cat(maxs).to(torch.float32).contiguous()
+
     def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
         """out: optional preallocated host (soft, mask) arrays for this rank's
         frames (the download lands there)."""
@@ -266,8 +293,7 @@ class ShardedSolver:
             io = self.b.step(params, it)
             self.b.before_exchange()
             self._exchange(io)
-            fs = self._gather(io.frame_sum, torch.float64)
-            fm = self._gather(io.frame_max, torch.float32)
+            fs, fm = self._gather_sums(io.frame_sum, io.frame_max)
             self.b.after_exchange()
             self.b.finalize(params, it, fs, fm)
         norms = self.b.norms(cfg.iterations)
@@ -287,7 +313,6 @@ class ShardedSolver:
             io = self.b.step(params, it)
             self.b.before_exchange()
             self._exchange(io)
-            fs = self._gather(io.frame_sum, torch.float64)
-            fm = self._gather(io.frame_max, torch.float32)
+            fs, fm = self._gather_sums(io.frame_sum, io.frame_max)
             self.b.after_exchange()
             self.b.finalize(params, it, fs, fm)
