@@ -66,6 +66,10 @@
 #ifndef SFK_MC_NXB
 #define SFK_MC_NXB 2
 #endif
+// A-warp register budget of the EXACT kind (B gets the rest of the SMSP)
+#ifndef SFK_MC_RAE
+#define SFK_MC_RAE 72
+#endif
 
 namespace sfk {
 
@@ -108,7 +112,7 @@ struct McGeom {
     // warps w and w + 4 share a lane quadrant and take half the columns each
     static constexpr int RW = NF * BR;
     static constexpr int TCOLS = K * RW <= 128 ? 256 : 512;
-    static constexpr int RA = 64;
+    static constexpr int RA = EXACT ? SFK_MC_RAE : 64;  // EXACT: three fields + separate roundings
     // setmaxnreg: every warp starts with the launch grant RPOOL (65536 / NT,
     // multiple of 8); an SMSP holds NWA / 4 A and NWB / 4 B warps, and B can
     // take only what A gives back (asking for more blocks forever)
