@@ -309,6 +309,22 @@ int sfseg_shard_norms(sfseg_ctx* ctx, int32_t count, double* norms);
 /* Soft iterate / mask of the rank's output frames; frac as threshold_final. */
 int sfseg_shard_download(sfseg_ctx* ctx, double frac, float* soft, uint8_t* mask, int32_t mem);
 
+/* Peer-memory halo exchange (replaces step 2). A shard exports where its two
+ * iterate buffers live (CUDA IPC handles, or raw device pointers when the
+ * neighbours are contexts of the same process); each rank opens its
+ * neighbours' exports once, after sfseg_shard_load, and from then on
+ * sfseg_shard_step itself writes the rt edge frames of every new iterate
+ * into the neighbours' halo frames with k_halo_push (SM stores over
+ * NVLink / NVSwitch peer memory, stream-ordered after the stencil), so the
+ * driver skips the send/recv. The neighbours must not start the next step
+ * before this rank's step: the per-iteration all-gather of step 3 orders it.
+ * Calling sfseg_shard_load again drops the peers. */
+#define SFSEG_SHARD_EXPORT_BYTES 176
+int sfseg_shard_export(sfseg_ctx* ctx, int32_t same_process, void* blob);
+/* lo / hi: the exports of rank-1 / rank+1 (NULL at the volume ends); the
+ * call replaces the previous peer set (NULL, NULL: back to send/recv). */
+int sfseg_shard_set_peers(sfseg_ctx* ctx, const void* lo_blob, const void* hi_blob);
+
 /* ---- explicit-affinity oracle on the GPU (oracle.hpp:76-107) -------------
  * Matrix-free fp64 versions of the reference's SparseAffinity path: every
  * entry M_ij = sp_i sp_j pair(i,j) G(j-i) is regenerated in the reference's

@@ -26,6 +26,7 @@ SFSEG_ERR_STATE = 7
 SFSEG_ERR_IO = 8
 SFSEG_ERR_FORMAT = 9
 SFSEG_ERR_CORRUPTION = 10
+SFSEG_SHARD_EXPORT_BYTES = 176
 
 SFSEG_ARITH_EXACT = 0
 SFSEG_ARITH_FAST = 1
@@ -194,6 +195,8 @@ _SIGS = {
                                        C.POINTER(C.c_double), _I32]),
     "sfseg_shard_download": (C.c_int, [_P, C.c_double, _P, _P, _I32]),
     "sfseg_shard_norms": (C.c_int, [_P, _I32, C.POINTER(C.c_double)]),
+    "sfseg_shard_export": (C.c_int, [_P, _I32, _P]),
+    "sfseg_shard_set_peers": (C.c_int, [_P, _P, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -112,6 +112,14 @@ __global__ void k_sq_acc(Vol q, Vol f, int first) {
     }
 }
 
+// Halo push of the time-sharded solve: the rank's edge frames of the new
+// iterate into a neighbour's halo frames (dst is peer memory: NVLink stores)
+__global__ void k_halo_push(const float4* __restrict__ src, float4* __restrict__ dst, size_t n4) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
 // pow_volume (engine.cpp:52-71): float(pow(double s, p)); p==0 -> 1, p==1 -> copy
 __global__ void k_pow(Vol s, Vol out, double p) {
     SFK_FOR_VOXELS(s, t, y, x) {

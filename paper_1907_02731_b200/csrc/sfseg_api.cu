@@ -489,6 +489,11 @@ struct sfseg_ctx {
     void* pin[2] = {nullptr, nullptr};  // sfseg_load_files: pinned file-read buffers
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     bool pin_used[2] = {false, false};  // pin_ev[b] marks a DMA still reading pin[b]
+    // peer-memory halo exchange (sfseg_shard_set_peers): the neighbours' two
+    // iterate buffers, their buffer frame origin, and whether we opened them by IPC
+    float* peer_y[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lo, hi][y index]
+    int peer_buf_t0[2] = {0, 0};
+    bool peer_ipc[2] = {false, false};
     float* q = nullptr;              // Q = sum_c f_c^2 of the channel set q_for (fused_mc.cuh)
     std::vector<float*> q_for;
     // dense staging for host transfers (one contiguous DMA, re-pitched on the
@@ -529,6 +534,17 @@ float* dalloc_vol(sfseg_ctx* c) {
     return p;
 }
 
+// forget the neighbours' iterate buffers (sfseg_shard_set_peers)
+void drop_peers(sfseg_ctx* c) {
+    for (int side = 0; side < 2; ++side) {
+        for (int b = 0; b < 2; ++b) {
+            if (c->peer_ipc[side] && c->peer_y[side][b]) cudaIpcCloseMemHandle(c->peer_y[side][b]);
+            c->peer_y[side][b] = nullptr;
+        }
+        c->peer_ipc[side] = false;
+    }
+}
+
 void release_problem(sfseg_ctx* c) {
     if (c->guard_applied)
         for (size_t i = 0; i < c->Fw.size(); ++i)
@@ -545,6 +561,7 @@ void release_problem(sfseg_ctx* c) {
     c->tmp.clear();
     dfree(c->q);
     c->q_for.clear();
+    drop_peers(c);
     if (c->stage) cudaFree(c->stage);
     if (c->dmask) cudaFree(c->dmask);
     c->stage = nullptr;
@@ -2015,6 +2032,7 @@ int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C
         if (!S || !F) fail(SFSEG_ERR_PARAMETER, "null input");
         if (out_t0 < 0 || out_t1 <= out_t0 || out_t1 > static_cast<int>(T) || halo < 0)
             fail(SFSEG_ERR_PARAMETER, "bad shard range");
+        drop_peers(c);  // a new shard layout: the peers must be set again
         if (out_t1 - out_t0 < halo && !(out_t0 == 0 && out_t1 == static_cast<int>(T)))
             fail(SFSEG_ERR_PARAMETER, "a shard must own at least `halo` frames");
         const int buf_t0 = std::max(0, out_t0 - halo);
@@ -2062,9 +2080,23 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
         launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST);
+        const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
+        // peer-memory halo push: my first / last rt output frames straight into
+        // the neighbours' halo frames of the same iterate buffer
+        const int nh = std::min(c->halo, c->Tout());
+        for (int side = 0; side < 2; ++side) {
+            float* peer = c->peer_y[side][dst];
+            if (!peer || nh == 0) continue;
+            const int g0 = side == 0 ? c->out_t0 : c->out_t1 - nh;  // global first frame sent
+            const float* from = c->y[dst] + static_cast<size_t>(g0 - c->buf_t0) * fr;
+            float* to = peer + static_cast<size_t>(g0 - c->peer_buf_t0[side]) * fr;
+            const size_t n4 = static_cast<size_t>(nh) * fr / 4;
+            sfk::k_halo_push<<<c->num_sms * 2, 256, 0, c->stream>>>(
+                reinterpret_cast<const float4*>(from), reinterpret_cast<float4*>(to), n4);
+            launched(c->stream, "k_halo_push");
+        }
         frame_sums(c);
         c->cur = dst;
-        const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
         float* y = c->y[dst];
         const int buf_t1 = c->buf_t0 + c->T;
         std::memset(io, 0, sizeof *io);
@@ -2085,6 +2117,76 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
         }
         io->frame_sum = c->frame_sum;
         io->frame_max = c->frame_max;
+    });
+}
+
+namespace {
+struct ShardExport {  // SFSEG_SHARD_EXPORT_BYTES
+    cudaIpcMemHandle_t h[2];
+    uint64_t ptr[2];
+    int32_t same_process, buf_t0, T, H, P, device;
+    int32_t pad[2];
+};
+static_assert(sizeof(ShardExport) == SFSEG_SHARD_EXPORT_BYTES, "export blob size");
+}  // namespace
+
+int sfseg_shard_export(sfseg_ctx* c, int32_t same_process, void* blob) {
+    return guarded([&] {
+        if (!c || !blob) fail(SFSEG_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (!c->resident || !c->y[0] || !c->y[1]) fail(SFSEG_ERR_STATE, "sfseg_shard_export before sfseg_shard_load");
+        ShardExport e;
+        std::memset(&e, 0, sizeof e);
+        for (int b = 0; b < 2; ++b) {
+            e.ptr[b] = reinterpret_cast<uint64_t>(c->y[b]);
+            if (!same_process) ck(cudaIpcGetMemHandle(&e.h[b], c->y[b]), "cudaIpcGetMemHandle");
+        }
+        e.same_process = same_process ? 1 : 0;
+        e.buf_t0 = c->buf_t0;
+        e.T = c->T;
+        e.H = c->H;
+        e.P = c->P;
+        e.device = c->device;
+        std::memcpy(blob, &e, sizeof e);
+    });
+}
+
+int sfseg_shard_set_peers(sfseg_ctx* c, const void* lo, const void* hi) {
+    return guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_shard_set_peers before sfseg_shard_load");
+        drop_peers(c);  // the call replaces the peer set (NULL, NULL: none)
+        const void* blobs[2] = {lo, hi};
+        for (int side = 0; side < 2; ++side) {
+            if (!blobs[side]) continue;
+            ShardExport e;
+            std::memcpy(&e, blobs[side], sizeof e);
+            if (e.H != c->H || e.P != c->P) fail(SFSEG_ERR_SHAPE, "peer shard has another frame shape");
+            // the peer's halo frames on my side must be my edge frames
+            const int nh = std::min(c->halo, c->Tout());
+            const int g0 = side == 0 ? c->out_t0 : c->out_t1 - nh;
+            if (g0 < e.buf_t0 || g0 + nh > e.buf_t0 + e.T)
+                fail(SFSEG_ERR_SHAPE, "peer shard buffer does not hold this rank's edge frames");
+            for (int b = 0; b < 2; ++b) {
+                if (e.same_process) {
+                    if (e.device != c->device) {
+                        const cudaError_t pe = cudaDeviceEnablePeerAccess(e.device, 0);
+                        if (pe != cudaErrorPeerAccessAlreadyEnabled) ck(pe, "cudaDeviceEnablePeerAccess");
+                        cudaGetLastError();
+                    }
+                    c->peer_y[side][b] = reinterpret_cast<float*>(e.ptr[b]);
+                } else {
+                    void* p = nullptr;
+                    ck(cudaIpcOpenMemHandle(&p, e.h[b], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+                    c->peer_y[side][b] = static_cast<float*>(p);
+                }
+            }
+            c->peer_buf_t0[side] = e.buf_t0;
+            c->peer_ipc[side] = !e.same_process;
+        }
     });
 }
 

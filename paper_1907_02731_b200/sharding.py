@@ -28,6 +28,7 @@ first) and every rank runs its own clips with its own context.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
@@ -148,6 +149,20 @@ class CudaBackend:
                       device_tensor(io.frame_sum, io.out_frames, "float64"),
                       device_tensor(io.frame_max, io.out_frames, "float32"))
 
+    def export(self, same_process: bool) -> bytes:
+        """Where this shard's iterate buffers live (CUDA IPC handles, or raw
+        pointers for contexts of the same process): sfseg_shard_export."""
+        blob = C.create_string_buffer(N.SFSEG_SHARD_EXPORT_BYTES)
+        N.check(self.lib.sfseg_shard_export(self.ctx.handle, int(same_process), blob))
+        return blob.raw
+
+    def set_peers(self, lo: Optional[bytes], hi: Optional[bytes]) -> None:
+        """From now on sfseg_shard_step pushes the edge frames into the
+        neighbours' halos itself (peer-memory stores): no send/recv."""
+        bl = C.create_string_buffer(lo, len(lo)) if lo else None
+        bh = C.create_string_buffer(hi, len(hi)) if hi else None
+        N.check(self.lib.sfseg_shard_set_peers(self.ctx.handle, bl, bh))
+
     def before_exchange(self):
         import torch
 
@@ -223,11 +238,37 @@ class ShardedSolver:
         self.b.load(T, H, W, S_local, F_local, x0_local, self.t0, self.t1, halo)
         self.tmax = max(shard_range(T, self.world, r)[1] - shard_range(T, self.world, r)[0]
                         for r in range(self.world))
+        self.p2p = False
+        if self.world > 1 and hasattr(self.b, "export") and os.environ.get("SFSEG_P2P", "1") != "0":
+            self._enable_p2p()
+
+    def _enable_p2p(self):
+        """Peer-memory halo exchange: every rank opens its neighbours' iterate
+        buffers (CUDA IPC) and the step kernel stream pushes the edge frames
+        into them. All-or-nothing across the group: if any rank cannot open
+        its peers, every rank keeps the NCCL send/recv."""
+        import torch
+        import torch.distributed as dist
+
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, self.b.export(False), group=self.group)
+        ok = 1
+        try:
+            self.b.set_peers(blobs[self.rank - 1] if self.rank > 0 else None,
+                             blobs[self.rank + 1] if self.rank + 1 < self.world else None)
+        except N.Error:
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        self.p2p = bool(flag.item())
+        if not self.p2p and ok:
+            self.b.set_peers(None, None)  # some rank failed: everyone stays on NCCL
 
     def _exchange(self, io: StepIO):
         import torch.distributed as dist
 
-        if self.world == 1:
+        if self.world == 1 or self.p2p:  # p2p: the step already pushed the halos
             return
         ops = []
         if io.send_lo is not None:  # my first frames -> rank-1's upper halo
@@ -265,9 +306,12 @@ class ShardedSolver:
         if self.world == 1:
             return frame_sum, frame_max
         n, tm = frame_sum.numel(), self.tmax
-        packed = torch.zeros(2 * tm, dtype=torch.float64, device=frame_sum.device)
+        dev = frame_sum.device
+        packed = torch.zeros(2 * tm, dtype=torch.float64, device=dev)
         packed[:n] = frame_sum
         packed[tm:tm + n] = frame_max.to(torch.float64)
+        if packed.is_cuda and dist.get_backend(self.group) != "nccl":
+            packed = packed.cpu()  # gloo gathers host tensors (tests: ranks sharing one GPU)
         try:
             allp = torch.empty(self.world * 2 * tm, dtype=torch.float64, device=packed.device)
             dist.all_gather_into_tensor(allp, packed, group=self.group)
@@ -280,7 +324,8 @@ class ShardedSolver:
             a, b = shard_range(self.T, self.world, r)
             sums.append(bufs[r][: b - a])
             maxs.append(bufs[r][tm: tm + b - a])
-        return torch.cat(sums).contiguous(), torch.cat(maxs).to(torch.float32).contiguous()
+        return (torch.cat(sums).to(dev).contiguous(),
+                torch.cat(maxs).to(torch.float32).to(dev).contiguous())
 
     def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
         """out: optional preallocated host (soft, mask) arrays for this rank's

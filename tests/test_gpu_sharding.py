@@ -64,3 +64,52 @@ def test_shards_match_single_context(world, arith, binarize, idx):
     assert np.array_equal(norms, [r.l2_norm_pre_normalize for r in ref.trace.iterations])
     for be, _, _ in ranks:
         be.close()
+
+
+@pytest.mark.parametrize("world,arith,idx", [(2, "fast", 1), (3, "exact", 1), (3, "fast", 2)])
+def test_peer_memory_halo_push_matches_single_context(world, arith, idx):
+    # sfseg_shard_set_peers: the step pushes its edge frames into the
+    # neighbours' halo frames itself (k_halo_push); the driver only gathers
+    # the per-frame sums. Contexts of one process stand in for the ranks
+    # (raw device pointers instead of IPC handles); the streams are ordered
+    # through the host-side gather exactly as the NCCL all-gather orders them.
+    prob = synth.config(idx, frames=12)[0]
+    fs, _ = prob.generate()
+    if idx != 1:
+        fs = E.FeatureSet(np.ascontiguousarray(fs.unary[:, :100, :150]),
+                          [np.ascontiguousarray(f[:, :100, :150]) for f in fs.pairwise])
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, "iterations": 5,
+                           "binarize_start": 3})
+    T, H, W = fs.unary.shape
+    halo = cfg.kernel.radii[0]
+    ranks = []
+    for r in range(world):
+        t0, t1 = shard_range(T, world, r)
+        b0, b1 = buffer_range(T, t0, t1, halo)
+        be = CudaBackend(0)
+        be.load(T, H, W, np.ascontiguousarray(fs.unary[b0:b1]),
+                [np.ascontiguousarray(f[b0:b1]) for f in fs.pairwise], None, t0, t1, halo)
+        be.cfg = cfg
+        ranks.append((be, t0, t1))
+    blobs = [be.export(True) for be, _, _ in ranks]
+    for r, (be, _, _) in enumerate(ranks):
+        be.set_peers(blobs[r - 1] if r > 0 else None, blobs[r + 1] if r + 1 < world else None)
+    params = cfg.to_params()
+    for it in range(1, cfg.iterations + 1):
+        ios = [be.step(params, it) for be, _, _ in ranks]
+        for be, _, _ in ranks:
+            be.before_exchange()
+        fsum = torch.cat([io.frame_sum for io in ios]).contiguous()
+        fmax = torch.cat([io.frame_max for io in ios]).contiguous()
+        for be, _, _ in ranks:
+            be.after_exchange()
+            be.finalize(params, it, fsum, fmax)
+    soft = np.concatenate([be.download(cfg.final_threshold, a, b)[0] for be, a, b in ranks])
+    ref = E.run(fs, cfg)
+    assert np.array_equal(soft, ref.soft)
+    norms = ranks[0][0].norms(cfg.iterations)
+    assert np.array_equal(norms, [r.l2_norm_pre_normalize for r in ref.trace.iterations])
+    # dropping the peers puts the halos back on the driver's send/recv
+    for be, _, _ in ranks:
+        be.set_peers(None, None)
+        be.close()
