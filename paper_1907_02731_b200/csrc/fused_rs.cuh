@@ -240,7 +240,10 @@ struct RsGeom {
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
-template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool TMR_, bool ACC>
+// PEER: the time-sharded instantiation that also stores its edge planes into
+// the neighbours' halo frames (a separate instantiation: the single-GPU
+// kernel does not carry the extra epilogue code)
+template <int RT, int R, int NWA, int STAGES, int TY_, int BR_, bool TMR_, bool ACC, bool PEER = false>
 __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT, SFK_RS_CPS)
     fused_step_rs(const __grid_constant__ FusedArgs a) {
     using G = RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>;
@@ -1113,6 +1116,23 @@ __global__ void __launch_bounds__(RsGeom<RT, R, NWA, STAGES, TY_, BR_, TMR_>::NT
                     }
                 }
                 if (bt == 0) SFK_T(ecnt, 11);
+                // time-sharded solve: the edge planes of this rank also go
+                // straight into the neighbours' halo frames (peer memory,
+                // coalesced 128-byte rows; rows past H are not written)
+                if (PEER && last) {
+#pragma unroll
+                    for (int side = 0; side < 2; ++side) {
+                        float* pb = a.peer[side];
+                        const bool edge = side == 0 ? to < a.out_t0 + a.peer_n : to >= a.out_t1 - a.peer_n;
+                        if (!pb || !edge) continue;
+                        const int oy = q.tile_y * TY + BR * wb, nr = a.H - oy;
+                        float* po = pb + (static_cast<size_t>(to - a.peer_t0[side]) * a.H + oy) * a.pitch +
+                                    q.tile_x * TX + lane;
+#pragma unroll
+                        for (int r = 0; r < BR; ++r)
+                            if (r < nr) po[static_cast<size_t>(r) * a.pitch] = v[r];
+                    }
+                }
                 ++ecnt;
                 if (last && !WRED) {
                     if constexpr (DEFRED) {

@@ -195,6 +195,8 @@ struct FusedVariant {
     int box_w, box_h;
     int slab_h = 8;  // rows of the recombination-operand / output TMA boxes
     int ctas_per_sm = 1;  // persistent grid = ctas_per_sm x SMs
+    bool rs = false;      // fused_rs.cuh (stores the sharded solve's edge planes to the peers)
+    void (*kernel_peer)(FusedArgs) = nullptr;  // rs: single-group step + peer edge stores
 };
 
 template <int RT, int R, int TY, int TX, bool FMA>
@@ -267,8 +269,10 @@ FusedVariant variant_rs() {
     v.threads = G::NT;
     v.slab_h = (SFK_RS_WIDE && !TMR) ? TY : 8;
     v.ctas_per_sm = SFK_RS_CPS;
+    v.rs = true;
     v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
     v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, true>;
+    v.kernel_peer = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
@@ -494,6 +498,8 @@ struct sfseg_ctx {
     float* peer_y[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lo, hi][y index]
     int peer_buf_t0[2] = {0, 0};
     bool peer_ipc[2] = {false, false};
+    int peer_push_dst = -1;         // y index the current shard step writes (-1: not a shard step)
+    bool pushed_in_kernel = false;  // the step kernel already stored the edge planes to the peers
     float* q = nullptr;              // Q = sum_c f_c^2 of the channel set q_for (fused_mc.cuh)
     std::vector<float*> q_for;
     // dense staging for host transfers (one contiguous DMA, re-pitched on the
@@ -882,6 +888,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
     const float inv_alpha = static_cast<float>(1.0 / alpha);
     const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx, fma);
     g_conv_count.fetch_add(3ull * Fch.size(), std::memory_order_relaxed);
+    c->pushed_in_kernel = false;
     const McVariant* mc = (fma && Fch.size() > 1) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
     if (mc) {
         launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc);
@@ -932,11 +939,23 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         static bool attr_set[64] = {};
         const int vidx = static_cast<int>(v - variants().data());
         if (!attr_set[vidx]) {
-            for (auto kfn : {v->kernel, v->kernel_acc})
+            for (auto kfn : {v->kernel, v->kernel_acc, v->kernel_peer ? v->kernel_peer : v->kernel})
                 ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(v->smem)),
                    "cudaFuncSetAttribute");
             attr_set[vidx] = true;
+        }
+        // the FAST stencil (fused_rs.cuh) pushes the sharded solve's edge
+        // planes to the peers itself; other kernels leave it to k_halo_push
+        c->pushed_in_kernel = false;
+        if (fma && c->peer_push_dst >= 0 && v->kernel_peer && Fch.size() == 1) {
+            const int nh = std::min(c->halo, c->Tout());
+            for (int side = 0; side < 2; ++side) {
+                a.peer[side] = c->peer_y[side][c->peer_push_dst];
+                a.peer_t0[side] = c->peer_buf_t0[side];
+            }
+            a.peer_n = nh;
+            c->pushed_in_kernel = a.peer[0] || a.peer[1];
         }
         for (size_t g = 0; g < Fch.size(); ++g) {
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
@@ -950,7 +969,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                 cudaEventCreate(&e1);
                 cudaEventRecord(e0, c->stream);
             }
-            launch_pdl(g == 0 ? v->kernel : v->kernel_acc, grid_n, v->threads, v->smem, c->stream, a);
+            launch_pdl(c->pushed_in_kernel ? v->kernel_peer : g == 0 ? v->kernel : v->kernel_acc, grid_n,
+                       v->threads, v->smem, c->stream, a);
             launched(c->stream, "fused_step launch");
             if (c->timing) {
                 cudaEventRecord(e1, c->stream);
@@ -2079,14 +2099,16 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
         ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
+        c->peer_push_dst = dst;
         launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST);
+        c->peer_push_dst = -1;
         const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
         // peer-memory halo push: my first / last rt output frames straight into
         // the neighbours' halo frames of the same iterate buffer
         const int nh = std::min(c->halo, c->Tout());
         for (int side = 0; side < 2; ++side) {
             float* peer = c->peer_y[side][dst];
-            if (!peer || nh == 0) continue;
+            if (!peer || nh == 0 || c->pushed_in_kernel) continue;
             const int g0 = side == 0 ? c->out_t0 : c->out_t1 - nh;  // global first frame sent
             const float* from = c->y[dst] + static_cast<size_t>(g0 - c->buf_t0) * fr;
             float* to = peer + static_cast<size_t>(g0 - c->peer_buf_t0[side]) * fr;

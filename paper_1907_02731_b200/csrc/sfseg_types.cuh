@@ -49,6 +49,13 @@ struct FusedArgs {
     float inv_alpha;
     float c_inv_alpha;  // C / alpha (fused_mc.cuh HEAD launch)
     float* u_out;       // u = S^p x at the output points (fused_mc.cuh HEAD launch writes it)
+    // time-sharded solve with peer-memory halos (fused_rs.cuh, last group):
+    // output planes [out_t0, out_t0 + peer_n) also go to peer[0] (rank-1's
+    // iterate buffer, frame origin peer_t0[0]) and [out_t1 - peer_n, out_t1)
+    // to peer[1]; nullptr = no neighbour / not pushed by the kernel
+    float* peer[2];
+    int peer_t0[2];
+    int peer_n;
     float one, zero;  // 1.0f / 0.0f at run time (keeps ptxas from contracting EXACT FFMA2 pairs)
     int T, H, W, pitch;
     int buf_t0;      // global frame of input buffer frame 0
