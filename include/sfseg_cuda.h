@@ -28,6 +28,8 @@
 #ifndef SFSEG_CUDA_H
 #define SFSEG_CUDA_H
 
+#include "sfseg_synth.h"
+
 #include <stddef.h>
 #include <stdint.h>
 
@@ -357,6 +359,21 @@ int sfseg_affinity_power_iteration(sfseg_ctx* ctx, uint32_t frames, uint32_t hei
                                    int32_t kind, const double* x0, int32_t max_iters, double tol,
                                    double* eigenvector, double* eigenvalue,
                                    int32_t* iterations_used, int32_t mem);
+
+/* ---- device-side synthetic problems ------------ */
+
+/* sfseg_synth_generate (include/sfseg_synth.h) with S, F[c] and mask_out
+ * (may be NULL) in DEVICE memory: each thread jumps the (stream, frame)
+ * xoshiro256** generator to its run of 1024 pixels (GF(2) jump matrices) and
+ * draws what the host generator draws there. Geometry, mask, uniform noise,
+ * channel means and clipping are bit-identical to the host generator;
+ * gaussian draws use the device log/cos (within one ulp of glibc), so a rare
+ * value differs by one float ulp. F is a HOST array of channels device
+ * pointers (channels <= 16). stream: a cudaStream_t or NULL; the call
+ * returns after the generation finished. Returns 0, -1 (bad spec) or -2
+ * (CUDA failure). */
+int sfseg_synth_generate_device(const sfseg_synth_spec* spec, float* S, float* const* F,
+                                uint8_t* mask_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -197,6 +197,7 @@ _SIGS = {
     "sfseg_shard_norms": (C.c_int, [_P, _I32, C.POINTER(C.c_double)]),
     "sfseg_shard_export": (C.c_int, [_P, _I32, _P]),
     "sfseg_shard_set_peers": (C.c_int, [_P, _P, _P]),
+    "sfseg_synth_generate_device": (C.c_int, [_P, _P, _P, _P, _P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

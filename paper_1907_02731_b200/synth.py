@@ -83,6 +83,34 @@ class Problem:
             raise ValueError("bad synthetic spec")
         return FeatureSet(S, list(F)), m
 
+    def generate_device(self, device="cuda", mask: bool = False):
+        """The same problem generated in HBM by sfseg_synth_generate_device
+        (libsfseg_cuda.so, include/sfseg_cuda.h): returns (S, [F_c], mask or
+        None) as torch tensors on ``device``. Bit-identical to generate()
+        except gaussian draws (device log/cos: a rare value one float ulp off)."""
+        import torch
+
+        from ._native import load_library
+
+        lib = load_library()
+        T, H, W = self.shape
+        dev = torch.device(device)
+        S = torch.empty((T, H, W), dtype=torch.float32, device=dev)
+        F = [torch.empty((T, H, W), dtype=torch.float32, device=dev) for _ in range(self.channels)]
+        m = torch.empty((T, H, W), dtype=torch.uint8, device=dev) if mask else None
+        fptr = (C.c_void_p * self.channels)(*[f.data_ptr() for f in F])
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream().cuda_stream
+            rc = lib.sfseg_synth_generate_device(C.byref(self.spec), C.c_void_p(S.data_ptr()),
+                                                 C.cast(fptr, C.c_void_p),
+                                                 C.c_void_p(m.data_ptr()) if m is not None else None,
+                                                 C.c_void_p(stream))
+        if rc == -1:
+            raise ValueError("bad synthetic spec")
+        if rc != 0:
+            raise RuntimeError("sfseg_synth_generate_device: CUDA failure")
+        return S, F, m
+
 
 def _ptr(a) -> int:
     if hasattr(a, "data_ptr"):
