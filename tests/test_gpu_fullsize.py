@@ -81,3 +81,54 @@ def test_full_c1_solve_matches_reference_global_loop(c1, arith):
     cos = float(np.dot(got.ravel(), want.ravel()) / (np.linalg.norm(got) * np.linalg.norm(want)))
     assert err <= 1e-4, err
     assert cos >= 1 - 1e-6, cos
+
+
+def _gates(got, want, frac):
+    """North-star gates on the final iterate plus the mask band, and the
+    scale-aware forms: error relative to max|x_ref| and a
+    mask band of 1e-4 * max."""
+    got = got.astype(np.float64)
+    want = want.astype(np.float64)
+    err = float(np.max(np.abs(got - want)))
+    cos = float(np.dot(got.ravel(), want.ravel()) / (np.linalg.norm(got) * np.linalg.norm(want)))
+    assert err <= 1e-4, err
+    assert cos >= 1 - 1e-6, cos
+    mx = float(want.max())
+    assert err <= 1e-3 * mx, (err, mx)
+    cut_g, cut_w = frac * float(got.max()), frac * mx
+    flips = (got > cut_g) != (want > cut_w)
+    assert np.all(np.abs(want[flips] - cut_w) <= 1e-4 * mx), int(flips.sum())
+
+
+@pytest.fixture(scope="module")
+def c2_ref():
+    # full c2: 80 x 480 x 854, C = 8, kernel 7 x 15 x 15 (sigma_t box), 30 iterations
+    prob = synth.config(2)[0]
+    fs, _ = prob.generate()
+    iters = prob.cfg.iterations
+    cfg = _cfg(prob, "exact", iterations=iters, binarize_start=iters + 1)
+    want = Reference().global_loop(fs.unary, fs.pairwise, cfg, iters, threads=THREADS)
+    return prob, fs, want
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_full_c2_solve_matches_reference_global_loop(c2_ref, arith):
+    prob, fs, want = c2_ref
+    iters = prob.cfg.iterations
+    cfg = _cfg(prob, arith, iterations=iters, binarize_start=iters + 1)
+    res = E.run(fs, cfg)
+    _gates(res.soft, want, cfg.final_threshold)
+
+
+@pytest.mark.parametrize("clip", [0, 8])  # one clip of each resolution
+def test_full_c3_clip_matches_reference_global_loop(clip):
+    # whole c3 clips (T, H, W drawn by the config's seed), kernel 5 x 9 x 9, 25 iterations
+    prob = synth.config(3)[clip]
+    fs, _ = prob.generate()
+    iters = prob.cfg.iterations
+    want = Reference().global_loop(fs.unary, fs.pairwise,
+                                   _cfg(prob, "exact", iterations=iters, binarize_start=iters + 1),
+                                   iters, threads=THREADS)
+    for arith in ("exact", "fast"):
+        cfg = _cfg(prob, arith, iterations=iters, binarize_start=iters + 1)
+        _gates(E.run(fs, cfg).soft, want, cfg.final_threshold)
