@@ -527,6 +527,15 @@ struct sfseg_ctx {
     // device) and the device mask of downloads
     float* stage = nullptr;
     size_t stage_elems = 0;
+    // pipelined host uploads (load_impl): a copy stream DMAs row chunks into a
+    // two-slot staging ring while the library stream re-pitches and validates
+    cudaStream_t cstream = nullptr;
+    float* ring[2] = {nullptr, nullptr};
+    size_t ring_elems = 0;
+    cudaEvent_t ring_up[2] = {nullptr, nullptr};  // chunk landed in ring[b]
+    cudaEvent_t ring_rp[2] = {nullptr, nullptr};  // ring[b] consumed by its re-pitch
+    int* vflags = nullptr;  // per-volume validation flags of a load
+    int vflags_n = 0;
     uint8_t* dmask = nullptr;
     size_t dmask_elems = 0;
     // timing
@@ -1203,8 +1212,89 @@ void solve_until_impl(sfseg_ctx* c, const sfseg_params* p, int first, int max_it
     *done = std::min(it, max_iter);
 }
 
+// Host volumes of a load, pipelined: chunks of rows go H2D on the copy stream
+// into a two-slot staging ring; the library stream re-pitches each chunk as
+// it lands and validates each volume as soon as its last chunk is in, so the
+// re-pitch/validation of one volume (and S^p, when the caller already knows
+// p: sfseg_run) runs under the DMA of the next. One flag read-back at the
+// end; errors are reported in load order (unary, pairwise channels, x0), as
+// the sequential form reports them.
+void load_pipelined(sfseg_ctx* c, const float* S, const float* const* F, const float* x0,
+                    double sp_hint) {
+    if (!c->cstream) ck(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking), "stream");
+    const size_t W = c->W, rows = static_cast<size_t>(c->T) * c->H;
+    const size_t chunk_rows = std::max<size_t>(1, (size_t(32) << 20) / (W * sizeof(float)));
+    const size_t need = std::min(rows, chunk_rows) * W;
+    if (c->ring_elems < need) {
+        for (int b = 0; b < 2; ++b) {
+            if (c->ring[b]) cudaFree(c->ring[b]);
+            c->ring[b] = nullptr;
+        }
+        c->ring_elems = 0;
+        for (int b = 0; b < 2; ++b) ck(cudaMalloc(&c->ring[b], need * sizeof(float)), "malloc ring");
+        c->ring_elems = need;
+    }
+    for (int b = 0; b < 2; ++b) {
+        if (!c->ring_up[b]) ck(cudaEventCreateWithFlags(&c->ring_up[b], cudaEventDisableTiming), "event");
+        if (!c->ring_rp[b]) ck(cudaEventCreateWithFlags(&c->ring_rp[b], cudaEventDisableTiming), "event");
+    }
+    const int nv = 1 + c->C + (x0 ? 1 : 0);
+    if (c->vflags_n < nv) {
+        if (c->vflags) cudaFree(c->vflags);
+        c->vflags = nullptr;
+        c->vflags_n = 0;
+        ck(cudaMalloc(&c->vflags, nv * sizeof(int)), "malloc flags");
+        c->vflags_n = nv;
+    }
+    ck(cudaMemsetAsync(c->vflags, 0, nv * sizeof(int), c->stream), "memset flags");
+    // the copy stream starts after everything already queued on the library
+    // stream (earlier users of the destination buffers)
+    ck(cudaEventRecord(c->ring_rp[0], c->stream), "event");
+    ck(cudaStreamWaitEvent(c->cstream, c->ring_rp[0], 0), "wait");
+    ck(cudaEventRecord(c->ring_rp[1], c->stream), "event");
+    int slot = 0;
+    auto one = [&](float* dst, const float* src, int vi, bool nonneg) {
+        for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+            const size_t nr = std::min(chunk_rows, rows - r0);
+            ck(cudaStreamWaitEvent(c->cstream, c->ring_rp[slot], 0), "wait");
+            ck(cudaMemcpyAsync(c->ring[slot], src + r0 * W, nr * W * sizeof(float),
+                               cudaMemcpyHostToDevice, c->cstream),
+               "upload volume");
+            ck(cudaEventRecord(c->ring_up[slot], c->cstream), "event");
+            ck(cudaStreamWaitEvent(c->stream, c->ring_up[slot], 0), "wait");
+            sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(c->ring[slot], c->W,
+                                                                  dst + r0 * c->P, c->P, nr, c->W);
+            launched(c->stream, "k_repitch");
+            ck(cudaEventRecord(c->ring_rp[slot], c->stream), "event");
+            slot ^= 1;
+        }
+        sfk::k_validate<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(dst), nonneg,
+                                                                        c->vflags + vi);
+        launched(c->stream, "k_validate");
+    };
+    one(c->S, S, 0, true);
+    if (!std::isnan(sp_hint)) ensure_sp(c, sp_hint);  // S^p under the DMA of the channels
+    for (int i = 0; i < c->C; ++i) one(c->F[i], F[i], 1 + i, false);
+    if (x0) one(c->x0, x0, 1 + c->C, true);
+    std::vector<int> h(nv, 0);
+    ck(cudaMemcpyAsync(h.data(), c->vflags, nv * sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+       "flags");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    for (int v = 0; v < nv; ++v) {
+        const std::string what = v == 0 ? "unary" : (v <= c->C ? "pairwise" : "x0");
+        if (h[v] & 1) {
+            c->sp_p = NAN;
+            fail(SFSEG_ERR_VALIDATION, what + " contains a non-finite value");
+        }
+        if (h[v] & 2) {
+            c->sp_p = NAN;
+            fail(SFSEG_ERR_VALIDATION, what + ": unary/solution volume contains a negative value");
+        }
+    }
+}
+
 void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
-               const float* const* F, const float* x0, int32_t mem) {
+               const float* const* F, const float* x0, int32_t mem, double sp_hint = NAN) {
     check_shape(T, H, W);
     if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
     if (!S || !F) fail(SFSEG_ERR_PARAMETER, "null input");
@@ -1219,15 +1309,19 @@ void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
     c->guard_applied = false;
     c->sp_p = NAN;
     c->cur = -1;
-    upload(c, c->S, S, mem);
-    for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
-    validate_vol(c, c->S, true, "unary");
-    for (int i = 0; i < C; ++i) validate_vol(c, c->F[i], false, "pairwise");
     c->has_x0 = x0 != nullptr;
-    if (x0) {
-        if (!c->x0) c->x0 = dalloc_vol(c);
-        upload(c, c->x0, x0, mem);
-        validate_vol(c, c->x0, true, "x0");
+    if (x0 && !c->x0) c->x0 = dalloc_vol(c);
+    if (mem == SFSEG_MEM_HOST && c->P != c->W) {
+        load_pipelined(c, S, F, x0, sp_hint);
+    } else {
+        upload(c, c->S, S, mem);
+        for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
+        validate_vol(c, c->S, true, "unary");
+        for (int i = 0; i < C; ++i) validate_vol(c, c->F[i], false, "pairwise");
+        if (x0) {
+            upload(c, c->x0, x0, mem);
+            validate_vol(c, c->x0, true, "x0");
+        }
     }
     c->resident = true;
     c->q_for.clear();  // channel contents changed
@@ -1697,6 +1791,13 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         if (c->sched_seg) cudaFree(c->sched_seg);
         if (c->sched_off) cudaFree(c->sched_off);
         for (auto e : c->ev) cudaEventDestroy(e);
+        for (int b = 0; b < 2; ++b) {
+            if (c->ring[b]) cudaFree(c->ring[b]);
+            if (c->ring_up[b]) cudaEventDestroy(c->ring_up[b]);
+            if (c->ring_rp[b]) cudaEventDestroy(c->ring_rp[b]);
+        }
+        if (c->vflags) cudaFree(c->vflags);
+        if (c->cstream) cudaStreamDestroy(c->cstream);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -1856,7 +1957,13 @@ int sfseg_run(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const
               uint8_t* mask, sfseg_iter_record* rec, int32_t mem) {
     int rc = sfseg_params_validate(p);
     if (rc) return rc;
-    rc = sfseg_load(c, T, H, W, C, S, F, x0, mem);
+    // sfseg_load, with p known: S^p is computed under the DMA of the channels
+    rc = guarded([&] {
+        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        load_impl(c, T, H, W, C, S, F, x0, mem, p->p);
+    });
     if (rc) return rc;
     rc = sfseg_solve(c, p, 1, p->iterations, rec);
     if (rc) return rc;
