@@ -147,7 +147,9 @@ void* sfseg_ctx_stream(sfseg_ctx* ctx);
 
 /* Uploads S (unary) and C pairwise channels, validates them on the device
  * (FeatureSet::validate, volume.cpp:72-93) and keeps them resident. x0 is
- * optional (NULL = start from S, engine.cpp:267-270). */
+ * optional (NULL = start from S, engine.cpp:267-270). A host pairwise pointer
+ * equal to unary (the feature is the unary volume, f = S) is uploaded once
+ * and copied on the device. */
 int sfseg_load(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
                int32_t channels, const float* unary, const float* const* pairwise,
                const float* x0, int32_t mem);

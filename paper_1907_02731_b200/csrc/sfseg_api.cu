@@ -1274,7 +1274,17 @@ void load_pipelined(sfseg_ctx* c, const float* S, const float* const* F, const f
     };
     one(c->S, S, 0, true);
     if (!std::isnan(sp_hint)) ensure_sp(c, sp_hint);  // S^p under the DMA of the channels
-    for (int i = 0; i < c->C; ++i) one(c->F[i], F[i], 1 + i, false);
+    for (int i = 0; i < c->C; ++i) {
+        if (F[i] == S) {
+            // the channel IS the unary volume (e.g. f = x0 = S, BASELINE c0/c1):
+            // one upload, a device copy, and the unary's (stricter) validation
+            ck(cudaMemcpyAsync(c->F[i], c->S, c->vol_elems() * sizeof(float),
+                               cudaMemcpyDeviceToDevice, c->stream),
+               "copy channel");
+            continue;
+        }
+        one(c->F[i], F[i], 1 + i, false);
+    }
     if (x0) one(c->x0, x0, 1 + c->C, true);
     std::vector<int> h(nv, 0);
     ck(cudaMemcpyAsync(h.data(), c->vflags, nv * sizeof(int), cudaMemcpyDeviceToHost, c->stream),

@@ -74,3 +74,18 @@ def test_pipelined_load_reports_the_first_bad_volume():
     F[0][0, 0, 0] = np.nan
     with pytest.raises(E.ValidationError, match="unary"):
         E.run(E.FeatureSet(S, F), cfg, ctx=E.Context(0))
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_feature_aliasing_unary_is_uploaded_once_same_result(arith):
+    # f = S passed as one host buffer (sfseg_load uploads it once and copies it
+    # on the device) == f passed as its own copy, bit for bit
+    S, F, cfg = _problem()
+    cfg.arith = arith
+    ctx = E.Context(0)
+    a = E.run(E.FeatureSet(S, [S, F[1]]), cfg, ctx=ctx).soft
+    b = E.run(E.FeatureSet(S, [S.copy(), F[1]]), cfg, ctx=ctx).soft
+    assert np.array_equal(a, b)
+    c = E.run(E.FeatureSet(S, [S]), cfg, ctx=ctx).soft
+    d = E.run(E.FeatureSet(S, [S.copy()]), cfg, ctx=E.Context(0)).soft
+    assert np.array_equal(c, d)
