@@ -1212,15 +1212,9 @@ void solve_until_impl(sfseg_ctx* c, const sfseg_params* p, int first, int max_it
     *done = std::min(it, max_iter);
 }
 
-// Host volumes of a load, pipelined: chunks of rows go H2D on the copy stream
-// into a two-slot staging ring; the library stream re-pitches each chunk as
-// it lands and validates each volume as soon as its last chunk is in, so the
-// re-pitch/validation of one volume (and S^p, when the caller already knows
-// p: sfseg_run) runs under the DMA of the next. One flag read-back at the
-// end; errors are reported in load order (unary, pairwise channels, x0), as
-// the sequential form reports them.
-void load_pipelined(sfseg_ctx* c, const float* S, const float* const* F, const float* x0,
-                    double sp_hint) {
+// The copy stream and the two-slot staging ring of pipelined host transfers;
+// returns the rows per chunk (32 MB chunks).
+size_t ensure_ring(sfseg_ctx* c) {
     if (!c->cstream) ck(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking), "stream");
     const size_t W = c->W, rows = static_cast<size_t>(c->T) * c->H;
     const size_t chunk_rows = std::max<size_t>(1, (size_t(32) << 20) / (W * sizeof(float)));
@@ -1238,6 +1232,20 @@ void load_pipelined(sfseg_ctx* c, const float* S, const float* const* F, const f
         if (!c->ring_up[b]) ck(cudaEventCreateWithFlags(&c->ring_up[b], cudaEventDisableTiming), "event");
         if (!c->ring_rp[b]) ck(cudaEventCreateWithFlags(&c->ring_rp[b], cudaEventDisableTiming), "event");
     }
+    return chunk_rows;
+}
+
+// Host volumes of a load, pipelined: chunks of rows go H2D on the copy stream
+// into a two-slot staging ring; the library stream re-pitches each chunk as
+// it lands and validates each volume as soon as its last chunk is in, so the
+// re-pitch/validation of one volume (and S^p, when the caller already knows
+// p: sfseg_run) runs under the DMA of the next. One flag read-back at the
+// end; errors are reported in load order (unary, pairwise channels, x0), as
+// the sequential form reports them.
+void load_pipelined(sfseg_ctx* c, const float* S, const float* const* F, const float* x0,
+                    double sp_hint) {
+    const size_t W = c->W, rows = static_cast<size_t>(c->T) * c->H;
+    const size_t chunk_rows = ensure_ring(c);
     const int nv = 1 + c->C + (x0 ? 1 : 0);
     if (c->vflags_n < nv) {
         if (c->vflags) cudaFree(c->vflags);
@@ -1492,6 +1500,38 @@ void mask_of(sfseg_ctx* c, float* v, double frac, uint8_t* mask, int32_t mem) {
     launched(c->stream, "k_mask");
     if (mem != SFSEG_MEM_DEVICE)
         ck(cudaMemcpyAsync(mask, dm, n, cudaMemcpyDeviceToHost, c->stream), "mask D2H");
+}
+
+// Soft iterate (and mask) to host memory, pipelined: the library stream
+// de-pitches row chunks into the staging ring and the copy stream moves each
+// chunk D2H as soon as it is ready; the max and mask kernels run on the
+// library stream under the first chunks' DMA. The library stream ends after
+// the last copy, so synchronising it covers the whole download.
+void download_pipelined(sfseg_ctx* c, float* soft, float* x, double frac, uint8_t* mask) {
+    const size_t W = c->W, rows = static_cast<size_t>(c->T) * c->H;
+    const size_t chunk_rows = ensure_ring(c);
+    int slot = 0, k = 0;
+    bool masked = mask == nullptr;
+    for (size_t r0 = 0; r0 < rows; r0 += chunk_rows, ++k) {
+        const size_t nr = std::min(chunk_rows, rows - r0);
+        ck(cudaStreamWaitEvent(c->stream, c->ring_rp[slot], 0), "wait");  // slot drained
+        sfk::k_repitch<<<c->num_sms * 8, 256, 0, c->stream>>>(x + r0 * c->P, c->P, c->ring[slot],
+                                                              c->W, nr, c->W);
+        launched(c->stream, "k_repitch");
+        ck(cudaEventRecord(c->ring_up[slot], c->stream), "event");
+        ck(cudaStreamWaitEvent(c->cstream, c->ring_up[slot], 0), "wait");
+        ck(cudaMemcpyAsync(soft + r0 * W, c->ring[slot], nr * W * sizeof(float),
+                           cudaMemcpyDeviceToHost, c->cstream),
+           "download volume");
+        ck(cudaEventRecord(c->ring_rp[slot], c->cstream), "event");
+        slot ^= 1;
+        if (k == 1 && !masked) {
+            mask_of(c, x, frac, mask, SFSEG_MEM_HOST);
+            masked = true;
+        }
+    }
+    if (!masked) mask_of(c, x, frac, mask, SFSEG_MEM_HOST);
+    ck(cudaStreamWaitEvent(c->stream, c->ring_rp[slot ^ 1], 0), "wait");  // the last copy
 }
 
 }  // namespace
@@ -1905,8 +1945,12 @@ int sfseg_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, int32_
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         float* x = tmp_vol(c, 0);
         materialize(c, x);
-        if (soft) download(c, soft, x, mem);
-        if (mask) mask_of(c, x, frac, mask, mem);
+        if (soft && mem == SFSEG_MEM_HOST && c->P != c->W) {
+            download_pipelined(c, soft, x, frac, mask);
+        } else {
+            if (soft) download(c, soft, x, mem);
+            if (mask) mask_of(c, x, frac, mask, mem);
+        }
         ck(cudaStreamSynchronize(c->stream), "download");
     });
 }
