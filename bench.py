@@ -237,11 +237,19 @@ def main():
     iters = cfg.iterations
     same = prob.spec.feature_mode == synth.FEAT_SAME  # f = x0 = S (c0, c1, c3)
 
-    # pinned host inputs, generated once (every rank generates the same seeded
-    # problem and keeps its frames)
-    S = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
-    F = [torch.empty((T, H, W), dtype=torch.float32, pin_memory=True) for _ in range(Cn)]
-    prob.generate(out=(S.numpy(), [f.numpy() for f in F]))
+    # pinned host inputs, generated once. A time-sharded rank generates only
+    # its buffer frames (own frames + halos): the generator is per frame, so
+    # the slab equals those frames of the whole volume, and c4's 34 GB never
+    # sits in one host process.
+    sharded_run = world > 1 or args.sharded
+    if sharded_run:
+        from paper_1907_02731_b200.sharding import buffer_range, shard_range
+        g0, g1 = buffer_range(T, *shard_range(T, world, rank), cfg.kernel.radii[0])
+    else:
+        g0, g1 = 0, T
+    S = torch.empty((g1 - g0, H, W), dtype=torch.float32, pin_memory=True)
+    F = [torch.empty((g1 - g0, H, W), dtype=torch.float32, pin_memory=True) for _ in range(Cn)]
+    prob.generate(out=(S.numpy(), [f.numpy() for f in F]), frame_range=(g0, g1))
 
     def barrier():
         torch.cuda.synchronize()
@@ -304,8 +312,8 @@ def main():
         solver = ShardedSolver(be, rank, world)
         t0, t1 = shard_range(T, world, rank)
         b0, b1 = buffer_range(T, t0, t1, halo)
-        dS = S[b0:b1].cuda()
-        dF = [f[b0:b1].cuda() for f in F]
+        dS = S[b0 - g0:b1 - g0].cuda()
+        dF = [f[b0 - g0:b1 - g0].cuda() for f in F]
         solver.load(T, H, W, dS, dF, None, halo)
         for _ in range(args.warmup):
             solver.solve_only(cfg)
@@ -378,8 +386,8 @@ def main():
         for i in range(args.e2e_steps + 1):
             barrier()
             t_0 = time.perf_counter()
-            dS = S[b0:b1].to("cuda", non_blocking=True)
-            dF = [f[b0:b1].to("cuda", non_blocking=True) for f in F]
+            dS = S[b0 - g0:b1 - g0].to("cuda", non_blocking=True)
+            dF = [f[b0 - g0:b1 - g0].to("cuda", non_blocking=True) for f in F]
             solver.load(T, H, W, dS, dF, None, halo)
             solver.run(cfg, out=(soft.numpy(), mask.numpy()))
             if i > 0:

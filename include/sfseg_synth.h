@@ -52,6 +52,13 @@ typedef struct sfseg_synth_spec {
 int sfseg_synth_generate(const sfseg_synth_spec* spec, float* S, float* const* F,
                          uint8_t* mask_out, int threads);
 
+/* Frames [t0, t1) of the same problem (every frame has its own generators,
+ * so a slab equals the matching frames of the whole volume bit for bit);
+ * S, F[c] and mask_out hold t1 - t0 frames. Used by time-sharded ranks that
+ * only need their own frames. Returns 0 or -1 (bad spec or range). */
+int sfseg_synth_generate_frames(const sfseg_synth_spec* spec, uint32_t t0, uint32_t t1, float* S,
+                                float* const* F, uint8_t* mask_out, int threads);
+
 /* The reference RNG stream, for pinning against rng.hpp. */
 void sfseg_synth_xoshiro_u64(uint64_t seed, uint64_t* out, size_t n);
 void sfseg_synth_xoshiro_gaussian(uint64_t seed, double* out, size_t n);

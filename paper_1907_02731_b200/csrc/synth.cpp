@@ -80,11 +80,18 @@ extern "C" {
 
 int sfseg_synth_generate(const sfseg_synth_spec* sp, float* S, float* const* F, uint8_t* mask_out,
                          int threads) {
+    if (!sp) return -1;
+    return sfseg_synth_generate_frames(sp, 0, sp->frames, S, F, mask_out, threads);
+}
+
+int sfseg_synth_generate_frames(const sfseg_synth_spec* sp, uint32_t t0, uint32_t t1, float* S,
+                                float* const* F, uint8_t* mask_out, int threads) {
     if (!sp || !S || sp->frames == 0 || sp->height == 0 || sp->width == 0) return -1;
+    if (t0 >= t1 || t1 > sp->frames) return -1;
     if (sp->objects < 1 || sp->objects > 8 || sp->channels < 1) return -1;
     if (sp->channels > 0 && !F) return -1;
     const sfseg_synth_spec spec = *sp;
-    const uint32_t T = spec.frames, H = spec.height, W = spec.width;
+    const uint32_t H = spec.height, W = spec.width;
     const size_t plane = static_cast<size_t>(H) * W;
 
     // object parameters from stream 1000
@@ -135,7 +142,7 @@ int sfseg_synth_generate(const sfseg_synth_spec* sp, float* S, float* const* F, 
                     }
                 }
         }
-        const size_t off = static_cast<size_t>(t) * plane;
+        const size_t off = static_cast<size_t>(t - t0) * plane;  // buffers hold frames [t0, t1)
         if (mask_out) std::memcpy(mask_out + off, ind.data(), plane);
         auto noisy = [&](uint64_t stream, int kind, double level, const double* src, float* dst) {
             Xoshiro r(derive_seed(spec.seed, stream, t));
@@ -173,11 +180,11 @@ int sfseg_synth_generate(const sfseg_synth_spec* sp, float* S, float* const* F, 
     };
 
     int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
-    nt = std::max(1, std::min<int>(nt, static_cast<int>(T)));
+    nt = std::max(1, std::min<int>(nt, static_cast<int>(t1 - t0)));
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w)
         pool.emplace_back([&, w] {
-            for (uint32_t t = w; t < T; t += nt) frame_job(t);
+            for (uint32_t t = t0 + w; t < t1; t += nt) frame_job(t);
         });
     for (auto& th : pool) th.join();
     return 0;

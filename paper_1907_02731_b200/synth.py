@@ -46,6 +46,9 @@ def _load():
         _lib.sfseg_synth_generate.restype = C.c_int
         _lib.sfseg_synth_generate.argtypes = [C.POINTER(SynthSpec), C.c_void_p, C.c_void_p,
                                               C.c_void_p, C.c_int]
+        _lib.sfseg_synth_generate_frames.restype = C.c_int
+        _lib.sfseg_synth_generate_frames.argtypes = [C.POINTER(SynthSpec), C.c_uint32, C.c_uint32,
+                                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib.sfseg_synth_xoshiro_u64.argtypes = [C.c_uint64, C.c_void_p, C.c_size_t]
         _lib.sfseg_synth_xoshiro_gaussian.argtypes = [C.c_uint64, C.c_void_p, C.c_size_t]
     return _lib
@@ -63,11 +66,15 @@ class Problem:
         T, H, W = self.shape
         return T * H * W
 
-    def generate(self, threads: int = 0, out=None, mask: bool = False):
+    def generate(self, threads: int = 0, out=None, mask: bool = False, frame_range=None):
         """Returns (FeatureSet of numpy arrays, mask or None). ``out`` may hold
-        preallocated (S, [F_c]) float32 arrays (e.g. pinned host memory)."""
+        preallocated (S, [F_c]) float32 arrays (e.g. pinned host memory).
+        ``frame_range=(t0, t1)`` generates only those frames (bit-identical to
+        the same frames of the whole volume; a time shard's slab)."""
         lib = _load()
         T, H, W = self.shape
+        t0, t1 = frame_range if frame_range is not None else (0, T)
+        T = t1 - t0
         if out is None:
             S = np.empty((T, H, W), np.float32)
             F = [np.empty((T, H, W), np.float32) for _ in range(self.channels)]
@@ -75,10 +82,10 @@ class Problem:
             S, F = out
         fptr = (C.c_void_p * self.channels)(*[_ptr(f) for f in F])
         m = np.empty((T, H, W), np.uint8) if mask else None
-        rc = lib.sfseg_synth_generate(C.byref(self.spec), C.c_void_p(_ptr(S)),
-                                      C.cast(fptr, C.c_void_p),
-                                      C.c_void_p(m.ctypes.data) if m is not None else None,
-                                      int(threads))
+        rc = lib.sfseg_synth_generate_frames(C.byref(self.spec), int(t0), int(t1), C.c_void_p(_ptr(S)),
+                                             C.cast(fptr, C.c_void_p),
+                                             C.c_void_p(m.ctypes.data) if m is not None else None,
+                                             int(threads))
         if rc != 0:
             raise ValueError("bad synthetic spec")
         return FeatureSet(S, list(F)), m

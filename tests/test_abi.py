@@ -133,3 +133,15 @@ def test_convergence_criterion_is_validated_on_the_host():
     fs = E.FeatureSet(np.zeros((2, 4, 4), np.float32), [np.zeros((2, 4, 4), np.float32)])
     with pytest.raises(E.ParameterError):
         E.run_until_converged(fs, E.SfsegConfig(), 1e-6, criterion="residual")
+
+
+@pytest.mark.parametrize("idx,frames,rng", [(1, 10, (3, 7)), (2, 6, (0, 2)), (4, 5, (2, 5))])
+def test_synth_frame_range_is_the_slab_of_the_whole_volume(idx, frames, rng):
+    # a time shard generates only its buffer frames (sfseg_synth_generate_frames)
+    prob = synth.config(idx, frames=frames)[0]
+    whole, m = prob.generate(mask=True)
+    part, pm = prob.generate(mask=True, frame_range=rng)
+    t0, t1 = rng
+    assert np.array_equal(part.unary, whole.unary[t0:t1])
+    assert all(np.array_equal(a, b[t0:t1]) for a, b in zip(part.pairwise, whole.pairwise))
+    assert np.array_equal(pm, m[t0:t1])
