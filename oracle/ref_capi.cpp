@@ -272,6 +272,32 @@ int sfref_global_loop(uint32_t T, uint32_t H, uint32_t W, int32_t C, const float
     REF_CATCH
 }
 
+// the same loop, with snapshots of the normalised iterate after each listed
+// iteration (ascending, 1-based) and the pre-normalisation norms
+int sfref_global_loop_ck(uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+                         const float* const* F, const sfseg_params* p, int threads,
+                         int32_t iterations, float* out, const int32_t* ck, int32_t nck,
+                         float* ck_out, double* norms) {
+    REF_TRY
+    const auto fs = features(T, H, W, C, S, F);
+    const auto cfg = to_cfg(p, threads);
+    sfseg::FeatureVolume x = fs.unary;
+    x.set_role(sfseg::VolumeRole::solution);
+    int32_t j = 0;
+    for (int32_t k = 1; k <= iterations; ++k) {
+        auto r = sfseg::normalize_l2(sfseg::sfseg_step(x, fs, cfg));
+        x = std::move(r.first);
+        if (norms) norms[k - 1] = r.second;
+        if (j < nck && ck[j] == k) {
+            std::memcpy(ck_out + static_cast<std::size_t>(j) * x.size(), x.data(), x.size() * sizeof(float));
+            ++j;
+        }
+    }
+    std::memcpy(out, x.data(), x.size() * sizeof(float));
+    return 0;
+    REF_CATCH
+}
+
 void sfref_xoshiro_u64(uint64_t seed, uint64_t* out, std::size_t n) {
     sfseg::Xoshiro256StarStar rng(seed);
     for (std::size_t i = 0; i < n; ++i) out[i] = rng.next_u64();

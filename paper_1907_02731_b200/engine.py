@@ -489,6 +489,39 @@ def run(features: FeatureSet, cfg: SfsegConfig, x0=None, reference=None, ground_
     return RunResult(soft, mask, trace)
 
 
+def run_once(features: FeatureSet, cfg: SfsegConfig, x0=None,
+             ctx: Optional[Context] = None) -> RunResult:
+    """sfseg::run (engine.cpp:247-348) as ONE C-ABI call, sfseg_run: load (S^p
+    computed under the channels' DMA), solve 1..iterations, download. This is
+    the entry point bench.py's e2e times. A channel that is the unary array
+    itself (f = S, as in BASELINE c0/c1/c3) is passed as the same pointer and
+    crosses the bus once."""
+    ctx = ctx or default_context()
+    p = cfg.to_params()
+    N.check(ctx._lib.sfseg_params_validate(C.byref(p)))
+    sb = _Buf(features.unary)
+    shape = _shape3(sb.shape)
+    if len(features.pairwise) == 0:
+        raise ValidationError("feature set needs at least one pairwise channel")
+    fbs = [sb if f is features.unary else _Buf(f, shape) for f in features.pairwise]
+    x0b = _Buf(x0, shape) if x0 is not None else None
+    mem = _same_mem([sb] + fbs + ([x0b] if x0b else []))
+    T, H, W = shape
+    soft = _empty_like(sb)
+    mask = _empty_like(sb, np.uint8)
+    ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
+    recs = (N.IterRecord * cfg.iterations)()
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_run(ctx.handle, T, H, W, len(fbs), sb.ptr,
+                                   C.cast(_channel_ptrs(fbs), C.c_void_p),
+                                   x0b.ptr if x0b else None, C.byref(p), ob.ptr, mb.ptr, recs, mem))
+    trace = RunTrace()
+    for r in recs:
+        trace.iterations.append(IterationRecord(r.iter, r.l2_norm_pre_normalize,
+                                                wall_time_s=r.wall_time_s))
+    return RunResult(soft, mask, trace)
+
+
 def run_until_converged(features: FeatureSet, cfg: SfsegConfig, tol: float,
                         criterion: str = "angle", max_iterations: Optional[int] = None,
                         x0=None, ctx: Optional[Context] = None):

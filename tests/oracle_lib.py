@@ -262,6 +262,23 @@ class Reference(_Base):
                                              C.c_int(threads), C.c_int32(iterations), _vp(out)))
         return out
 
+    def global_loop_ck(self, S, F, cfg, iterations, checkpoints, threads=1):
+        """global_loop plus the normalised iterate after each checkpoint
+        iteration and the pre-normalisation norms: (final, snaps, norms)"""
+        S = np.ascontiguousarray(S, _F)
+        F = [np.ascontiguousarray(f, _F) for f in F]
+        T, H, W = S.shape
+        out = np.empty_like(S)
+        ck = np.asarray(sorted(checkpoints), np.int32)
+        snaps = np.empty((len(ck),) + S.shape, _F)
+        norms = np.zeros(iterations)
+        p = params(cfg)
+        self._chk(self.lib.sfref_global_loop_ck(
+            C.c_uint32(T), C.c_uint32(H), C.c_uint32(W), C.c_int32(len(F)), _vp(S),
+            C.cast(_chans(F), C.c_void_p), C.byref(p), C.c_int(threads), C.c_int32(iterations),
+            _vp(out), _vp(ck), C.c_int32(len(ck)), _vp(snaps), _vp(norms)))
+        return out, {int(k): snaps[i] for i, k in enumerate(ck)}, norms
+
     def xoshiro_u64(self, seed, n):
         out = np.empty(n, np.uint64)
         self.lib.sfref_xoshiro_u64(C.c_uint64(seed), _vp(out), C.c_size_t(n))

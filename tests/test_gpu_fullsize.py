@@ -8,9 +8,11 @@ size-independent properties of the operator:
     power of two), EXACT and FAST
   * symmetry: the affinity matrix is symmetric (oracle.cpp:67-175), so
     <x, M y> == <M x, y> up to fp32 rounding, EXACT and FAST
-  * the whole c1 workload (30 iterations, binarisation off) against the
-    reference's normalize_l2(sfseg_step) loop (bench.cpp:154-155), which
-    run() equals bit for bit (test_engine.cpp:276-297): north-star gates
+  * the whole c1 and c2 workloads (30 iterations, binarisation off) against
+    the reference's normalize_l2(sfseg_step) loop (bench.cpp:154-155), which
+    run() equals bit for bit (test_engine.cpp:276-297): north-star gates and
+    the scale-aware forms at every checkpoint (1, 5, 10, 20, 30) and on the
+    final iterate and mask
 """
 import os
 
@@ -69,18 +71,35 @@ def test_full_c1_operator_is_symmetric(c1, arith):
     assert abs(a - b) <= 1e-6 * abs(a), (a, b)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast"])
-def test_full_c1_solve_matches_reference_global_loop(c1, arith):
+@pytest.fixture(scope="module")
+def c1_ref(c1):
     prob, fs = c1
     iters = prob.cfg.iterations  # 30
+    cfg = _cfg(prob, "exact", iterations=iters, binarize_start=iters + 1)
+    return Reference().global_loop_ck(fs.unary, fs.pairwise, cfg, iters, CKS, threads=THREADS)
+
+
+CKS = (1, 5, 10, 20, 30)
+
+
+def _run_checkpoints(fs, cfg):
+    snaps = {}
+    res = E.run(fs, cfg, observer=lambda it, x: snaps.__setitem__(it, x.copy()) if it in CKS else None)
+    return res, snaps
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_full_c1_solve_matches_reference_global_loop(c1, c1_ref, arith):
+    prob, fs = c1
+    want, ref_snaps, norms = c1_ref
+    iters = prob.cfg.iterations
     cfg = _cfg(prob, arith, iterations=iters, binarize_start=iters + 1)
-    res = E.run(fs, cfg)
-    want = Reference().global_loop(fs.unary, fs.pairwise, cfg, iters, threads=THREADS).astype(np.float64)
-    got = res.soft.astype(np.float64)
-    err = float(np.max(np.abs(got - want)))
-    cos = float(np.dot(got.ravel(), want.ravel()) / (np.linalg.norm(got) * np.linalg.norm(want)))
-    assert err <= 1e-4, err
-    assert cos >= 1 - 1e-6, cos
+    res, snaps = _run_checkpoints(fs, cfg)
+    for it in CKS:  # every checkpointed iteration (north star)
+        _gates(snaps[it], ref_snaps[it], cfg.final_threshold)
+    _gates(res.soft, want, cfg.final_threshold)
+    mine = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
+    assert np.allclose(mine, norms, rtol=1e-9 if arith == "exact" else 1e-5)
 
 
 def _gates(got, want, frac):
@@ -107,17 +126,21 @@ def c2_ref():
     fs, _ = prob.generate()
     iters = prob.cfg.iterations
     cfg = _cfg(prob, "exact", iterations=iters, binarize_start=iters + 1)
-    want = Reference().global_loop(fs.unary, fs.pairwise, cfg, iters, threads=THREADS)
+    want = Reference().global_loop_ck(fs.unary, fs.pairwise, cfg, iters, CKS, threads=THREADS)
     return prob, fs, want
 
 
 @pytest.mark.parametrize("arith", ["exact", "fast"])
 def test_full_c2_solve_matches_reference_global_loop(c2_ref, arith):
-    prob, fs, want = c2_ref
+    prob, fs, (want, ref_snaps, norms) = c2_ref
     iters = prob.cfg.iterations
     cfg = _cfg(prob, arith, iterations=iters, binarize_start=iters + 1)
-    res = E.run(fs, cfg)
+    res, snaps = _run_checkpoints(fs, cfg)
+    for it in CKS:
+        _gates(snaps[it], ref_snaps[it], cfg.final_threshold)
     _gates(res.soft, want, cfg.final_threshold)
+    mine = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
+    assert np.allclose(mine, norms, rtol=1e-9 if arith == "exact" else 1e-5)
 
 
 @pytest.mark.parametrize("clip", [0, 8])  # one clip of each resolution
