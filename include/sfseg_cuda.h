@@ -140,6 +140,10 @@ int sfseg_ctx_synchronize(sfseg_ctx* ctx);
  * recorded since timing was enabled or since the last call, and their count;
  * consumes the records. Used to time time-sharded solves (sfseg_shard_step). */
 int sfseg_ctx_kernel_time(sfseg_ctx* ctx, double* ms, int32_t* launches);
+/* Measured FP32 FMA-pipe throughput of the device in TFLOP/s (best of 3
+ * timed runs of an FFMA2 stream kernel): the denominator of the FP32
+ * roofline the multi-channel configs are bound by (bench.py). */
+int sfseg_probe_fp32_peak(int device, double* tflops);
 /* The context's cudaStream_t (as void*), for ordering NCCL work against it. */
 void* sfseg_ctx_stream(sfseg_ctx* ctx);
 

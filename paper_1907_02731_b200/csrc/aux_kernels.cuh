@@ -8,6 +8,7 @@
 
 #include "device_common.cuh"
 #include "sfseg_types.cuh"
+#include "step_common.cuh"  // Arith
 
 namespace sfk {
 
@@ -111,6 +112,42 @@ __global__ void k_sq_acc(Vol q, Vol f, int first) {
         const float v = f.p[i];
         q.p[i] = first ? v * v : fmaf(v, v, q.p[i]);
     }
+}
+
+// u = S^p T(x) for the multi-channel FAST step (fused_mc.cuh reads U boxes):
+// T = identity at iteration 1 (x = S or x0) and in normalise mode (FAST
+// applies 1/||y|| at the output), the FAST sigmoid in binarised iterations
+// (engine.cpp:92-100, 185-205). The same product the kernel's old in-box
+// form computed, bit for bit. Also k_make_u's output of a step's last
+// launch (write_u) is the same S^p * y.
+__global__ void k_make_u(Vol xv, Vol sp, Vol u, const IterState* __restrict__ st) {
+    griddep_wait();  // PDL: the previous finalize wrote st
+    const bool sig = st->mode == 2;
+    const IterState s = *st;
+    SFK_FOR_VOXELS(u, t, y, x) {
+        const size_t i = u.at(t, y, x);
+        const float v = xv.p[i];
+        u.p[i] = sp.p[i] * (sig ? Arith<true>::load_sigmoid(v, s) : v);
+    }
+}
+
+// FP32 FMA-pipe peak probe (sfseg_probe_fp32_peak): 8 independent FFMA2
+// chains per thread with a broadcast multiplier, the stencils' instruction
+// form; 2 lanes x 2 flops per FFMA2 lane-pair
+__global__ void k_fma_probe(float* out, float seed, int iters) {
+    float2 a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = make_float2(seed + threadIdx.x + j, seed - j);
+    const float2 m = make_float2(seed * 0.999f, seed * 0.999f);
+    const float2 c = make_float2(seed * 1e-3f, seed * 2e-3f);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = ffma2(a[j], m, c);
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
+    if (s == 1234.5f) out[threadIdx.x] = s;  // keeps the chains live
 }
 
 // Halo push of the time-sharded solve: the rank's edge frames of the new

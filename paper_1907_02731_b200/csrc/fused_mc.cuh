@@ -11,14 +11,24 @@
 // so a step needs C + 2 convolved fields instead of the 1 + 2C of the
 // per-channel form (c2, C = 8: 10 fields instead of 24; c4, C = 3: 5 instead
 // of 9). All of them in one pass would need a t-pass ring of
-// (2 RT + 1) x (C + 2) planes per output tile (c2: 573 KB for a 64 x 32 tile),
-// which no on-chip memory holds, so the fields run in groups of NF <= 2 per
-// launch, each a single pass over the volume:
+// (2 RT + 1) x (C + 2) planes per output tile (c4: 368 KB for a 64 x 32 tile),
+// more than the 256 KB of tensor memory, so the fields run in groups, each a
+// single pass over the volume:
 //
-//   HEAD (first launch): raw boxes x, S^p, Q; fields u and Q u;
-//        y  = S^p ((C/alpha - Q) G(u) - G(Q u)); also writes u to U
-//   TAIL (later launches): raw boxes U, f_a [, f_b]; fields f_a u [, f_b u];
-//        y += 2 S^p (f_a G(f_a u) + f_b G(f_b u))
+//   HEAD (first launch, NF = 2 or 3): raw boxes U, Q [, f_1]; fields u, Q u
+//        [, f_1 u]; y = S^p ((C/alpha - Q) G(u) - G(Q u) [+ 2 f_1 G(f_1 u)])
+//   TAIL (later launches, NF = 1 or 2): raw boxes U, f_a [, f_b]; fields
+//        f_a u [, f_b u]; y += 2 S^p (f_a G(f_a u) + f_b G(f_b u))
+//
+// c4 (C = 3) is HEAD(3) + TAIL(2): two passes per iteration.
+//
+// U = S^p x is the u field itself. The last launch of a step writes, instead
+// of y_{k+1}, U_{k+1} = S^p y_{k+1} (write_u) whenever the next iteration
+// only normalises (FAST defers the 1/||y|| to the output, so u_{k+1} is
+// exactly S^p y_{k+1}): the next step then reads one box (U) where it would
+// read two (x, S^p), and HBM sees the same bytes per iteration. The first
+// iteration, a sigmoid iteration (which needs the reduction first) and the
+// last iteration of a solve (the caller reads y) go through y and k_make_u.
 //
 // The schedule, roles and pipeline are those of fused_step_rs (fused_rs.cuh)
 // with its t-pass ring in tensor memory: one 512-thread CTA per SM walking
@@ -44,31 +54,13 @@
 #include <type_traits>
 
 #include "device_common.cuh"
-#include "fused_step.cuh"  // PlaneStream, Arith, ffma2
+#include "step_common.cuh"  // PlaneStream, Arith, ffma2, canonical_tree32
 #include "sfseg_types.cuh"
 
-// ablation bits (development builds, tools/ablate.sh): 1 A x-pass arithmetic
-// off, 2 B y-pass off, 4 t-pass ring loads off, 8 recombination/store off
-#ifndef SFK_MC_EXP
-#define SFK_MC_EXP 0
-#endif
-// SFK_MC_TB: t-pass ring slots loaded per tcgen05.wait::ld batch
+
+// ring slots fetched per tcgen05.wait::ld in the t-pass
 #ifndef SFK_MC_TB
 #define SFK_MC_TB 1
-#endif
-// x-pass (A) warps, TMA box stages, x-pass buffers
-#ifndef SFK_MC_NWA
-#define SFK_MC_NWA 8
-#endif
-#ifndef SFK_MC_STAGES
-#define SFK_MC_STAGES 2
-#endif
-#ifndef SFK_MC_NXB
-#define SFK_MC_NXB 2
-#endif
-// A-warp register budget of the EXACT kind (B gets the rest of the SMSP)
-#ifndef SFK_MC_RAE
-#define SFK_MC_RAE 72
 #endif
 
 namespace sfk {
@@ -78,7 +70,7 @@ enum McKind { MC_HEAD = 0, MC_TAIL = 1, MC_EXACT = 2 };
 template <int RT, int R, int NF, int KIND>
 struct McGeom {
     static constexpr bool HEAD = KIND == MC_HEAD, EXACT = KIND == MC_EXACT;
-    static constexpr int TY = 64, TX = 32, BR = 8, NWA = SFK_MC_NWA, NWB = TY / BR, STAGES = SFK_MC_STAGES;
+    static constexpr int TY = 64, TX = 32, BR = 8, NWA = 8, NWB = TY / BR, STAGES = 2;
     static constexpr int NA = 32 * NWA, NB = 32 * NWB, NT = NA + NB;
     static constexpr int K = 2 * RT + 1;
     static constexpr int BH = TY + 2 * R;
@@ -87,8 +79,8 @@ struct McGeom {
     static constexpr int BW = TX + HX + HR, BW4 = BW / 4;
     static constexpr int XOFF = HX - R;
     static constexpr int FB = (BH * BW + 31) / 32 * 32;
-    // raw boxes: HEAD x, S^p, Q; TAIL U, f_a [, f_b]; EXACT x, S^p, f
-    static constexpr int NR = EXACT ? 3 : NF + 1;
+    // raw boxes: HEAD U, Q [, f_1]; TAIL U, f_a [, f_b]; EXACT x, S^p, f
+    static constexpr int NR = EXACT ? 3 : HEAD ? NF : NF + 1;
     static constexpr int SW = 8;
     static constexpr int NINX = SW + 2 * R;
     static constexpr int NLD = (XOFF + NINX + 3) / 4;
@@ -96,11 +88,12 @@ struct McGeom {
     static constexpr int XPASS = (RBLK + NWA - 1) / NWA;
     static constexpr int TXU = TX + 4;
     static constexpr int XBU = (BH * TXU + 31) / 32 * 32;  // one field of the x-pass output
-    static constexpr int NXB = SFK_MC_NXB;
-    // recombination operands (TMA slabs, one emitted plane ahead): S^p, Q |
-    // S^p, f_a [, f_b], y of the earlier launches
+    static constexpr int NXB = 2;
+    // recombination operands (TMA slabs, one emitted plane ahead): S^p, Q
+    // [, f_1] | S^p, f_a [, f_b], y of the earlier launches
     // (EXACT: S^p, f, y of the earlier channels)
-    static constexpr int NOP = HEAD ? 2 : EXACT ? 3 : NF + 2;
+    static constexpr int NOP = HEAD ? NF : EXACT ? 3 : NF + 2;
+    static constexpr int NFC = HEAD ? NF - 1 : EXACT ? 1 : NF;  // channel-type slabs after S^p
     static constexpr int SLAB = BR * TX;
     static constexpr size_t RAW_FLOATS = size_t(STAGES) * NR * FB;
     static constexpr size_t XB_FLOATS = size_t(NXB) * NF * XBU;
@@ -112,7 +105,7 @@ struct McGeom {
     // warps w and w + 4 share a lane quadrant and take half the columns each
     static constexpr int RW = NF * BR;
     static constexpr int TCOLS = K * RW <= 128 ? 256 : 512;
-    static constexpr int RA = EXACT ? SFK_MC_RAE : 64;  // EXACT: three fields + separate roundings
+    static constexpr int RA = EXACT ? 72 : 64;  // EXACT: three fields + separate roundings
     // setmaxnreg: every warp starts with the launch grant RPOOL (65536 / NT,
     // multiple of 8); an SMSP holds NWA / 4 A and NWB / 4 B warps, and B can
     // take only what A gives back (asking for more blocks forever)
@@ -123,7 +116,7 @@ struct McGeom {
     static_assert((TXU / 4) % 2 == 1, "conflict-free x-pass rows");
     static_assert(BW <= 256 && BH <= 256, "TMA box limit");
     static_assert(K * RW <= TCOLS / 2, "TMEM ring of one thread");
-    static_assert(EXACT ? NF == 3 : (NF >= 1 && NF <= 2 && (NF == 2 || !HEAD)), "field groups");
+    static_assert(EXACT ? NF == 3 : HEAD ? (NF == 2 || NF == 3) : (NF == 1 || NF == 2), "field groups");
     static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
     static_assert(NWA % 4 == 0 && NWB % 4 == 0, "setmaxnreg acts on whole warpgroups");
 };
@@ -155,7 +148,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 
     const int tid = threadIdx.x;
     griddep_wait();  // PDL: the previous step / finalize has completed
-    if (a.st->degenerate && SFK_MC_EXP == 0) return;  // an earlier iteration hit a zero norm
+    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;
 
@@ -169,7 +162,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
         for (int w = 0; w < NWB; ++w) mbar_init(&slab_full[w], 1);
         fence_barrier_init();
         prefetch_tensormap(&a.tm_x);
-        if (HEAD) prefetch_tensormap(&a.tm_sp);
+        if (EXACT) prefetch_tensormap(&a.tm_sp);
         prefetch_tensormap(&a.tm_f[0]);
         prefetch_tensormap(&a.tm_out);
         prefetch_tensormap(&a.tm_spc);
@@ -215,8 +208,8 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
             uint64_t* bar = &raw_full[s];
             const int bx = pq.tile_x * TX - G::HX, by = pq.tile_y * TY - R, bt = tg - a.buf_t0;
             if (pbox == 0) mbar_arrive_expect_tx(bar, NR * BH * BW * sizeof(float));
-            const CUtensorMap* map = pbox == 0 ? &a.tm_x : (HEAD || EXACT) ? (pbox == 1 ? &a.tm_sp : &a.tm_f[0])
-                                                                        : &a.tm_f[pbox - 1];
+            const CUtensorMap* map = pbox == 0 ? &a.tm_x : EXACT ? (pbox == 1 ? &a.tm_sp : &a.tm_f[0])
+                                                                 : &a.tm_f[pbox - 1];
             tma_load_3d(dst, map, bar, bx, by, bt);
             ++pcount;
             pq.next();
@@ -225,16 +218,17 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
             pq.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
             for (int s = 0; s < STAGES; ++s) issue_box();
         }
-        const bool sigm = (HEAD || EXACT) && st.mode == 2;
+        // FAST reads U = S^p T(x) (k_make_u or the previous step's write_u)
+        const bool sigm = EXACT && st.mode == 2;
         const bool norm = EXACT && st.mode == 1;  // EXACT normalises on load
         const int xw = tid >> 5, xl = tid & 31;  // lane -> (row xl & 7, strip xl >> 3)
 
         // one x-pass item: box row r, strip sx (SW outputs as column pairs)
-        auto item = [&](auto sig_c, const float* rs, float* xbb, int r, int sx, float* urow) {
-            constexpr bool SIG = decltype(sig_c)::value == 2, NRM = decltype(sig_c)::value == 1;
+        auto item = [&](auto sig_c, const float* rs, float* xbb, int r, int sx) {
+            [[maybe_unused]] constexpr bool SIG = decltype(sig_c)::value == 2;
+            [[maybe_unused]] constexpr bool NRM = decltype(sig_c)::value == 1;
             const float4* py = reinterpret_cast<const float4*>(rs) + r * BW4 + 2 * sx;
             float2 ou[NF][SW / 2];
-            float uc[SW];  // HEAD: u at this strip's own points (for U)
             float4 v[NR];
 #pragma unroll
             for (int m4 = 0; m4 < G::NLD * 4; ++m4) {
@@ -257,11 +251,10 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                     phi[1] = xmul(e4[2], u);
                     phi[2] = xmul(xmul(e4[2], e4[2]), u);
                 } else if constexpr (HEAD) {
-                    const float x = SIG ? A::load_sigmoid(e4[0], st) : e4[0];
-                    const float u = e4[1] * x;  // engine.cpp:92-100
+                    const float u = e4[0];  // U = S^p x (engine.cpp:92-100)
                     phi[0] = u;
-                    phi[1] = e4[2] * u;  // Q u
-                    if (m >= R && m < R + SW) uc[m - R] = u;
+                    phi[1] = e4[1] * u;  // Q u
+                    if constexpr (NF > 2) phi[2] = e4[2] * u;  // f_1 u
                 } else {
 #pragma unroll
                     for (int i = 0; i < NF; ++i) phi[i] = e4[1 + i] * e4[0];  // f_i u
@@ -273,6 +266,18 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                         const int e = m - 2 * k;
                         if (e < 0 || e > 2 * R + 1) continue;
                         // x-pass starts from acc = 0 (conv3d.cpp:92): 0 + p = p
+                        if constexpr (!EXACT) {
+                            // the pair's two edge taps have a zero partner
+                            // (w[-1], w[2R+1]): one scalar op instead of FFMA2
+                            if (e == 0) {
+                                ou[i][k] = make_float2(phi[i] * a.taps_x[0], 0.0f);
+                                continue;
+                            }
+                            if (e == 2 * R + 1) {
+                                ou[i][k].y = fmaf(phi[i], a.taps_x[2 * R], ou[i][k].y);
+                                continue;
+                            }
+                        }
                         ou[i][k] = acc2(ou[i][k], make_float2(phi[i], phi[i]), a.tpair_x[e], e == 0);
                     }
                 }
@@ -283,13 +288,6 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 #pragma unroll
                 for (int w = 0; w < SW / 4; ++w)
                     du[w] = make_float4(ou[i][2 * w].x, ou[i][2 * w].y, ou[i][2 * w + 1].x, ou[i][2 * w + 1].y);
-            }
-            if constexpr (HEAD) {
-                if (urow) {
-                    float4* pu = reinterpret_cast<float4*>(urow + sx * SW);
-                    pu[0] = make_float4(uc[0], uc[1], uc[2], uc[3]);
-                    pu[1] = make_float4(uc[4], uc[5], uc[6], uc[7]);
-                }
             }
         };
 
@@ -310,23 +308,16 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                 const int blk = xw + k * G::NWA;
                 if (blk >= G::RBLK) break;
                 const int r = blk * 8 + (xl & 7);
-                if (r >= BH || (SFK_MC_EXP & 1)) continue;
-                float* urow = nullptr;  // HEAD: U row of this item's output points
-                if constexpr (HEAD) {
-                    const int oy = q.tile_y * TY + r - R;
-                    if (r >= R && r < R + TY && oy < a.H)
-                        urow = a.u_out + (static_cast<size_t>(tg - a.buf_t0) * a.H + oy) * a.pitch +
-                               q.tile_x * TX;
-                }
+                if (r >= BH) continue;
                 using L0 = std::integral_constant<int, 0>;
                 using L1 = std::integral_constant<int, 1>;
                 using L2 = std::integral_constant<int, 2>;
-                if (sigm)
-                    item(L2{}, rs, xbb, r, xl >> 3, urow);
+                if (EXACT && sigm)
+                    item(L2{}, rs, xbb, r, xl >> 3);
                 else if (EXACT && norm)
-                    item(L1{}, rs, xbb, r, xl >> 3, urow);
+                    item(L1{}, rs, xbb, r, xl >> 3);
                 else
-                    item(L0{}, rs, xbb, r, xl >> 3, urow);
+                    item(L0{}, rs, xbb, r, xl >> 3);
             }
             mbar_arrive(&xb_full[b]);  // release: this thread's x-pass stores
             named_bar_sync(1, NA);     // raw stage s fully read
@@ -367,7 +358,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
             const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
             tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
 #pragma unroll
-            for (int i = 0; i < ((HEAD || EXACT) ? 1 : NF); ++i)
+            for (int i = 0; i < G::NFC; ++i)
                 tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
             if (yprev)  // y so far: written by the previous launch (stream order)
                 tma_load_3d(slab + (NOP - 1) * SLAB, &a.tm_out, sfull, x, y, t + a.buf_t0 - a.out_buf_t0);
@@ -392,7 +383,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                 const int b = cnt % NXB;
                 mbar_wait(&xb_full[b], (cnt / NXB) & 1);
 #pragma unroll
-                for (int i = 0; i < ((SFK_MC_EXP & 2) ? 0 : NF); ++i) {
+                for (int i = 0; i < NF; ++i) {
                     const float* xc = xb + (static_cast<size_t>(b) * NF + i) * XBU + (BR * wb) * TXU + lane;
                     float vin[BR + 2 * R];
 #pragma unroll
@@ -400,14 +391,22 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 #pragma unroll
                     for (int e = 0; e <= 2 * R + 1; ++e) {
 #pragma unroll
-                        for (int k = 0; k < BR / 2; ++k)
-                            cur[i][k] = acc2(cur[i][k], make_float2(vin[2 * k + e], vin[2 * k + e]),
-                                             a.tpair_y[e], e == 0);
+                        for (int k = 0; k < BR / 2; ++k) {
+                            const float vv = vin[2 * k + e];
+                            if constexpr (!EXACT) {  // zero-partner edge taps as scalar ops
+                                if (e == 0) {
+                                    cur[i][k] = make_float2(vv * a.taps_y[0], 0.0f);
+                                    continue;
+                                }
+                                if (e == 2 * R + 1) {
+                                    cur[i][k].y = fmaf(vv, a.taps_y[2 * R], cur[i][k].y);
+                                    continue;
+                                }
+                            }
+                            cur[i][k] = acc2(cur[i][k], make_float2(vv, vv), a.tpair_y[e], e == 0);
+                        }
                     }
                 }
-                if (SFK_MC_EXP & 2)
-                    for (int i = 0; i < NF; ++i)
-                        for (int k = 0; k < BR / 2; ++k) cur[i][k] = make_float2(xb[lane], xb[lane + 32]);
                 mbar_arrive(&xb_empty[b]);
                 ++cnt;
             } else {
@@ -420,20 +419,20 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                 // t-pass (conv3d.cpp:147-165): K - 1 ring slots (oldest first), then this plane
                 float2 tacc[NF][BR / 2];
                 tmem_wait_st();
-                constexpr int TB = SFK_MC_TB;
+                constexpr int TB = SFK_MC_TB;  // ring slots per tcgen05.wait::ld
 #pragma unroll
                 for (int d0 = 0; d0 < K; d0 += TB) {
                     float w[TB][NF][8];
 #pragma unroll
                     for (int j = 0; j < TB; ++j) {
                         const int d = d0 + j;
-                        if (d >= K - 1 || (SFK_MC_EXP & 4)) continue;
+                        if (d >= K - 1) continue;
                         int sl = rslot + 1 + d;
                         sl = sl >= K ? sl - K : sl;
 #pragma unroll
                         for (int i = 0; i < NF; ++i) tmem_ld8(tm_ring + sl * RW + 8 * i, w[j][i]);
                     }
-                    if (d0 < K - 1 && !(SFK_MC_EXP & 4)) tmem_wait_ld();
+                    if (d0 < K - 1) tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < TB; ++j) {
                         const int d = d0 + j;
@@ -443,7 +442,7 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                         for (int i = 0; i < NF; ++i)
 #pragma unroll
                             for (int k = 0; k < BR / 2; ++k) {
-                                const float2 lu = (d == K - 1 || (SFK_MC_EXP & 4))
+                                const float2 lu = d == K - 1
                                                       ? cur[i][k]
                                                       : make_float2(w[j][i][2 * k], w[j][i][2 * k + 1]);
                                 tacc[i][k] = acc2(tacc[i][k], lu, w2, d == 0);
@@ -465,10 +464,6 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                 float v[BR];
 #pragma unroll
                 for (int r = 0; r < BR; ++r) {
-                    if (SFK_MC_EXP & 8) {
-                        v[r] = tacc[0][r / 2].x;
-                        continue;
-                    }
                     float g[NF];
 #pragma unroll
                     for (int i = 0; i < NF; ++i) g[i] = (r & 1) ? tacc[i][r / 2].y : tacc[i][r / 2].x;
@@ -477,8 +472,10 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                         const float term = A::recombine(opv[0][r], opv[1][r], a.inv_alpha, g[0], g[2], g[1]);
                         v[r] = first ? term : xadd(opv[2][r], term);
                     } else if constexpr (HEAD) {
-                        // S^p ((C/alpha - Q) G(u) - G(Q u))
-                        v[r] = (opv[0][r] * scale) * ((a.c_inv_alpha - opv[1][r]) * g[0] - g[1]);
+                        // S^p ((C/alpha - Q) G(u) - G(Q u) [+ 2 f_1 G(f_1 u)])
+                        float h = (a.c_inv_alpha - opv[1][r]) * g[0] - g[1];
+                        if constexpr (NF > 2) h = fmaf(2.0f * opv[2][r], g[2], h);
+                        v[r] = (opv[0][r] * scale) * h;
                     } else {
                         // 2 S^p sum_i f_i G(f_i u)
                         float sfg = opv[1][r] * g[0];
@@ -490,12 +487,14 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 #pragma unroll
                     for (int r = 0; r < BR; ++r) v[r] += opv[NOP - 1][r];
                 }
-                // y_{k+1} rows -> staging -> TMA store (clipped at the volume edge)
+                // y_{k+1} rows (or U_{k+1} = S^p y_{k+1}) -> staging -> TMA
+                // store (clipped at the volume edge)
                 float* ost = slab + NOP * SLAB;
                 if (lane == 0) bulk_wait_read0();  // the previous store has read the staging
                 __syncwarp();
+                const bool wu = !EXACT && last && a.write_u;
 #pragma unroll
-                for (int r = 0; r < BR; ++r) ost[r * TX + lane] = v[r];
+                for (int r = 0; r < BR; ++r) ost[r * TX + lane] = wu ? opv[0][r] * v[r] : v[r];
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {

@@ -30,7 +30,7 @@
 #include <type_traits>
 
 #include "device_common.cuh"
-#include "fused_step.cuh"  // PlaneStream, Arith, ffma2
+#include "step_common.cuh"  // PlaneStream, Arith, ffma2, canonical_tree32
 #include "fused_ws.cuh"    // SFK_T timeline instrumentation
 #include "sfseg_types.cuh"
 

@@ -30,7 +30,7 @@
 #include <type_traits>
 
 #include "device_common.cuh"
-#include "fused_step.cuh"  // PlaneStream, Arith, canonical_tree32, SFK_RING_SWITCH
+#include "step_common.cuh"  // PlaneStream, Arith, ffma2, canonical_tree32
 #include "sfseg_types.cuh"
 
 // ablation builds (tools/ablate.sh): bit 0 drops A's arithmetic, bit 1 B's;

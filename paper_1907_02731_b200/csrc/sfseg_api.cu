@@ -3,7 +3,7 @@
 //
 // Per iteration of Algorithm 1 (engine.cpp:284-341) the context launches, on
 // its own stream: the fused stencil kernel once per channel group
-// (fused_step.cuh), k_finalize_frames and k_finalize_total. No host
+// (fused_rs.cuh / fused_ws.cuh / fused_mc.cuh) and k_finalize. No host
 // synchronisation happens inside the loop; norms and the projection scalars
 // stay on the device (IterState) until the solve ends.
 #include <cuda.h>
@@ -23,7 +23,7 @@
 
 #include "../../include/sfseg_cuda.h"
 #include "aux_kernels.cuh"
-#include "fused_step.cuh"
+#include "step_common.cuh"
 #include "fused_ws.cuh"
 #include "fused_rs.cuh"
 #include "fused_mc.cuh"
@@ -199,25 +199,6 @@ struct FusedVariant {
     void (*kernel_peer)(FusedArgs) = nullptr;  // rs: single-group step + peer edge stores
 };
 
-template <int RT, int R, int TY, int TX, bool FMA>
-FusedVariant variant() {
-    constexpr int QY = 4, ST = 2;
-    using G = sfk::FusedGeom<RT, R, 1, TY, TX, QY, ST>;
-    FusedVariant v;
-    v.rt = RT;
-    v.r = R;
-    v.ty = TY;
-    v.tx = TX;
-    v.fma = FMA;
-    v.smem = G::SMEM_BYTES;
-    v.threads = G::NT;
-    v.kernel = sfk::fused_step<RT, R, 1, TY, TX, QY, ST, FMA>;
-    v.kernel_acc = v.kernel;
-    v.box_w = G::BW;
-    v.box_h = G::BH;
-    return v;
-}
-
 #ifndef SFK_NWA
 #define SFK_NWA 8
 #endif
@@ -271,7 +252,7 @@ FusedVariant variant_rs() {
     v.ctas_per_sm = SFK_RS_CPS;
     v.rs = true;
     v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
-    v.kernel_acc = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, true>;
+    v.kernel_acc = nullptr;  // FAST with C > 1 runs fused_mc.cuh (every rs radius has an mc variant)
     v.kernel_peer = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
@@ -284,21 +265,22 @@ FusedVariant variant_rs() {
     variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>(),       \
         variant_rs<3, 7, 2, true, 8, 64, 8>(), variant_rs<4, 10, 2, true, 8, 64, 8>()
 
-// FAST, C > 1: (C + 2)-field launches (fused_mc.cuh): a HEAD (u, Q u) and
-// TAILs of one or two channels (f_a u [, f_b u])
+// FAST, C > 1: (C + 2)-field launches (fused_mc.cuh): a HEAD (u, Q u, f_1 u)
+// and TAILs of one or two channels (f_a u [, f_b u])
 struct McVariant {
     int rt, r;
     int threads, box_w, box_h;
     size_t smem[4];          // head, tail of 2 channels, tail of 1, EXACT per channel
     void (*kernel[4])(FusedArgs);
 };
+constexpr int kHeadChannels = 1;  // channels folded into the HEAD launch (f_1 u)
 
 template <int RT, int R>
 McVariant variant_mc() {
     McVariant v;
     v.rt = RT;
     v.r = R;
-    using GH = sfk::McGeom<RT, R, 2, sfk::MC_HEAD>;
+    using GH = sfk::McGeom<RT, R, 3, sfk::MC_HEAD>;
     using G2 = sfk::McGeom<RT, R, 2, sfk::MC_TAIL>;
     using G1 = sfk::McGeom<RT, R, 1, sfk::MC_TAIL>;
     using GE = sfk::McGeom<RT, R, 3, sfk::MC_EXACT>;
@@ -309,7 +291,7 @@ McVariant variant_mc() {
     v.smem[1] = G2::SMEM_BYTES;
     v.smem[2] = G1::SMEM_BYTES;
     v.smem[3] = GE::SMEM_BYTES;
-    v.kernel[0] = sfk::fused_step_mc<RT, R, 2, sfk::MC_HEAD>;
+    v.kernel[0] = sfk::fused_step_mc<RT, R, 3, sfk::MC_HEAD>;
     v.kernel[1] = sfk::fused_step_mc<RT, R, 2, sfk::MC_TAIL>;
     v.kernel[2] = sfk::fused_step_mc<RT, R, 1, sfk::MC_TAIL>;
     v.kernel[3] = sfk::fused_step_mc<RT, R, 3, sfk::MC_EXACT>;
@@ -325,23 +307,11 @@ const std::vector<McVariant>& mc_variants() {
     variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \
         variant_ws<2, 5, FMA_>()
 
-#define SFK_VARIANTS(FMA_)                                                                \
-    variant<1, 2, 48, 32, FMA_>(), variant<1, 3, 48, 32, FMA_>(),                        \
-        variant<2, 4, 48, 32, FMA_>(), variant<2, 5, 48, 32, FMA_>()
-
-// Default: EXACT runs the warp-specialised kernel (fused_ws.cuh), FAST the
-// register-streamed one (fused_rs.cuh). SFSEG_KERNEL=ws runs fused_ws for
-// FAST too, SFSEG_KERNEL=v4 the single-role kernel (fused_step.cuh); both
-// are kept for comparison.
+// EXACT runs the warp-specialised kernel (fused_ws.cuh), FAST the
+// register-streamed one (fused_rs.cuh).
 const std::vector<FusedVariant>& variants() {
-    static const std::string which = [] {
-        const char* e = std::getenv("SFSEG_KERNEL");
-        return std::string(e ? e : "");
-    }();
-    static const std::vector<FusedVariant> rs = {SFK_VARIANTS_WS(false), SFK_VARIANTS_RS()};
-    static const std::vector<FusedVariant> ws = {SFK_VARIANTS_WS(false), SFK_VARIANTS_WS(true)};
-    static const std::vector<FusedVariant> old = {SFK_VARIANTS(false), SFK_VARIANTS(true)};
-    return which == "v4" ? old : which == "ws" ? ws : rs;
+    static const std::vector<FusedVariant> v = {SFK_VARIANTS_WS(false), SFK_VARIANTS_RS()};
+    return v;
 }
 
 // Host scheduler for the persistent stencil grid: G CTAs, ntiles tiles of
@@ -361,28 +331,7 @@ Schedule build_schedule(int ntiles, int tout, int G) {
     const int k1 = ntiles / G, rem = ntiles % G;
     for (int b = 0; b < G; ++b)
         for (int j = 0; j < k1; ++j) per[b].push_back(make_int4(j * G + b, 0, tout, 0));
-    static const bool even = [] {
-        const char* e = std::getenv("SFSEG_SCHED");
-        return e && std::string(e) == "even";
-    }();
-    if (rem > 0 && even) {
-        // SFSEG_SCHED=even: the rem leftover tiles' frames, concatenated tile
-        // by tile, cut into G equal pieces (a piece crossing a tile boundary
-        // becomes two segments, the second starting at frame 0). Measured
-        // (tools/sched_ab.sh): c1 FAST 212 vs 206 us per launch, c2 229 vs
-        // 218: the balanced pieces sweep neighbouring tiles at different
-        // frames, so their halo rows no longer meet in L2. Off.
-        const long long total = static_cast<long long>(rem) * tout;
-        for (int b = 0; b < G; ++b) {
-            long long p0 = total * b / G, p1 = total * (b + 1) / G;
-            while (p0 < p1) {
-                const int r = static_cast<int>(p0 / tout), t0 = static_cast<int>(p0 % tout);
-                const int t1 = static_cast<int>(std::min<long long>(tout, t0 + (p1 - p0)));
-                per[b].push_back(make_int4(k1 * G + r, t0, t1, 0));
-                p0 += t1 - t0;
-            }
-        }
-    } else if (rem > 0) {
+    if (rem > 0) {
         int c = std::max(1, std::min(G / rem, tout));
         const int L = (tout + c - 1) / c;
         c = (tout + L - 1) / L;
@@ -418,13 +367,8 @@ const FusedVariant* pick_variant(int rt, int ry, int rx, bool fma) {
     return best;
 }
 
-// SFSEG_MC=0 keeps the per-channel launches for FAST multi-channel steps
 const McVariant* pick_mc(int rt, int ry, int rx) {
-    static const bool off = [] {
-        const char* e = std::getenv("SFSEG_MC");
-        return e && *e == '0';
-    }();
-    if (off || env_flag("SFSEG_FORCE_GENERIC")) return nullptr;
+    if (env_flag("SFSEG_FORCE_GENERIC")) return nullptr;
     const int r = std::max(ry, rx);
     const McVariant* best = nullptr;
     for (const auto& v : mc_variants())
@@ -487,6 +431,7 @@ struct sfseg_ctx {
     float* x0 = nullptr;
     float* y[2] = {nullptr, nullptr};
     int cur = -1;                // index into y of the current raw iterate (-1: none)
+    bool cur_u = false;          // y[cur] holds U = S^p y (fused_mc.cuh write_u), not y
     double sp_p = NAN;           // p that sp was computed for
     // scratch
     double* part = nullptr;
@@ -613,6 +558,7 @@ void release_problem(sfseg_ctx* c) {
     c->loaded = false;
     c->resident = false;
     c->cur = -1;
+    c->cur_u = false;
     c->sp_p = NAN;
     c->guard_applied = false;
 }
@@ -782,6 +728,19 @@ void upload_schedule(sfseg_ctx* c, int ntiles, int tout, int G) {
     c->sched_key = key;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to a device's context:
+// set once per (device, kernel), thread-safe, before the first launch
+void ensure_smem_attr(sfseg_ctx* c, void (*fn)(FusedArgs), size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, void (*)(FusedArgs)>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& d : done)
+        if (d.first == c->device && d.second == fn) return;
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+       "cudaFuncSetAttribute");
+    done.emplace_back(c->device, fn);
+}
+
 void fill_taps(FusedArgs& a, const HostKernel& k, const FusedVariant& v) {
     std::memset(a.taps_x, 0, sizeof a.taps_x);
     std::memset(a.taps_y, 0, sizeof a.taps_y);
@@ -816,13 +775,24 @@ float* ensure_q(sfseg_ctx* c, const std::vector<float*>& Fch) {
 }
 
 // FAST step for C > 1 channels in the (C + 2)-field form (fused_mc.cuh): a
-// HEAD launch (u, Q u; writes u) and ceil(C / 2) TAIL launches of one or two
-// channels accumulating into y; the last launch emits the reductions
+// HEAD launch (u, Q u, f_1 u) and ceil((C - 1) / 2) TAIL launches of one or
+// two channels accumulating into y; the last launch emits the reductions and
+// stores U_{k+1} = S^p y_{k+1} instead of y_{k+1} when write_u. The u field
+// is read from x_src when src_is_u (the previous step stored U), else made
+// by k_make_u. EXACT (exact = true): one launch per channel, the reference's
+// per-channel form.
 void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
                     const IterState* st, float* out, const std::vector<float*>& Fch,
-                    const McVariant& v, bool exact = false) {
+                    const McVariant& v, bool exact, bool src_is_u, bool write_u) {
     float* q = exact ? nullptr : ensure_q(c, Fch);
-    float* u = exact ? nullptr : tmp_vol(c, 0);
+    const float* u = x_src;
+    if (!exact && !src_is_u) {
+        float* ub = tmp_vol(c, 0);
+        launch_pdl(sfk::k_make_u, aux_grid(c), sfk::kAuxThreads, 0, c->stream, c->vol(const_cast<float*>(x_src)),
+                   c->vol(c->sp), c->vol(ub), st);
+        launched(c->stream, "k_make_u");
+        u = ub;
+    }
     FusedVariant fv;  // taps / tensor-map geometry
     fv.rt = v.rt;
     fv.r = v.r;
@@ -835,7 +805,6 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
     a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, fv.tx, 8);
     a.sp = c->sp;
     a.out = out;
-    a.u_out = u;
     a.part = c->part;
     a.frame_max = c->frame_max;
     a.part_t0 = c->out_t0;
@@ -861,17 +830,9 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
     upload_schedule(c, a.tiles_x * a.tiles_y, c->Tout(), grid_n);
     a.sched = c->sched_seg;
     a.sched_off = c->sched_off;
-    static bool attr_set[16] = {};
-    const int vidx = static_cast<int>(&v - mc_variants().data());
-    if (!attr_set[vidx]) {
-        for (int i = 0; i < 4; ++i)
-            ck(cudaFuncSetAttribute(v.kernel[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(v.smem[i])),
-               "cudaFuncSetAttribute");
-        attr_set[vidx] = true;
-    }
+    for (int i = 0; i < 4; ++i) ensure_smem_attr(c, v.kernel[i], v.smem[i]);
     const int C = static_cast<int>(Fch.size());
-    const int ntail = exact ? C - 1 : (C + 1) / 2;
+    const int ntail = exact ? C - 1 : (C - kHeadChannels + 1) / 2;
     for (int g = 0; g <= ntail; ++g) {
         int kind = 0;
         if (exact) {  // one launch per channel: boxes x, S^p, f_g; operands S^p, f_g, y
@@ -879,14 +840,15 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
             a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, fv.tx, 8);
-        } else if (g == 0) {
-            a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+        } else if (g == 0) {  // boxes U, Q, f_1; operands S^p, Q, f_1
+            a.tm_x = make_tmap(u, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(q, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(q, c->T, c->H, c->W, c->P, fv.tx, 8);
-        } else {
-            const int c0 = 2 * (g - 1), n = std::min(2, C - c0);
+            a.tm_f[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+            a.tm_fc[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, fv.tx, 8);
+        } else {  // boxes U, f_a [, f_b]; operands S^p, f_a [, f_b], y
+            const int c0 = kHeadChannels + 2 * (g - 1), n = std::min(2, C - c0);
             kind = n == 2 ? 1 : 2;
-            if (g == 1) a.tm_x = make_tmap(u, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             for (int i = 0; i < n; ++i) {
                 a.tm_f[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
                 a.tm_fc[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, fv.tx, 8);
@@ -894,6 +856,7 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
         }
         a.first_group = g == 0;
         a.last_group = g == ntail;
+        a.write_u = !exact && g == ntail && write_u;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (c->timing) {
             cudaEventCreate(&e0);
@@ -913,24 +876,28 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
 // One step y_out = sum_c step_c(T(x_src)) with fused kernels or the generic
 // multi-pass path; emits canonical partials + frame max into c->part /
 // c->frame_max for the whole volume.
-void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
-                 const IterState* st, float* out, const std::vector<float*>& Fch, bool fma) {
+// src_is_u: x_src holds U = S^p x (a previous FAST multi-channel step stored
+// it); write_u: the step may store U_{k+1} instead of y_{k+1}. Returns
+// whether it did (only the multi-channel FAST path does).
+bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x_src,
+                 const IterState* st, float* out, const std::vector<float*>& Fch, bool fma,
+                 bool src_is_u = false, bool write_u = false) {
     const float inv_alpha = static_cast<float>(1.0 / alpha);
     const FusedVariant* v = pick_variant(k.rt, k.ry, k.rx, fma);
     g_conv_count.fetch_add(3ull * Fch.size(), std::memory_order_relaxed);
     c->pushed_in_kernel = false;
     const McVariant* mc = (fma && Fch.size() > 1) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
     if (mc) {
-        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc);
-        return;
+        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc, false, src_is_u, write_u);
+        return write_u;
     }
+    if (src_is_u) fail(SFSEG_ERR_STATE, "iterate stored as S^p y for another step path");
     // EXACT beyond the warp-specialised instantiations (c2, c4 radii): the
     // per-channel EXACT launches of fused_mc.cuh
-    static const bool exact_mc = env_flag("SFSEG_EXACT_MC");  // prefer it over fused_ws too
-    const McVariant* mce = (!fma && (!v || exact_mc)) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
+    const McVariant* mce = (!fma && !v) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
     if (mce) {
-        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mce, true);
-        return;
+        launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mce, true, false, false);
+        return false;
     }
     if (v) {
         FusedArgs a;
@@ -966,15 +933,8 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         upload_schedule(c, ntiles, c->Tout(), grid_n);
         a.sched = c->sched_seg;
         a.sched_off = c->sched_off;
-        static bool attr_set[64] = {};
-        const int vidx = static_cast<int>(v - variants().data());
-        if (!attr_set[vidx]) {
-            for (auto kfn : {v->kernel, v->kernel_acc, v->kernel_peer ? v->kernel_peer : v->kernel})
-                ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(v->smem)),
-                   "cudaFuncSetAttribute");
-            attr_set[vidx] = true;
-        }
+        for (auto kfn : {v->kernel, v->kernel_acc, v->kernel_peer})
+            if (kfn) ensure_smem_attr(c, kfn, v->smem);
         // the FAST stencil (fused_rs.cuh) pushes the sharded solve's edge
         // planes to the peers itself; other kernels leave it to k_halo_push
         c->pushed_in_kernel = false;
@@ -987,6 +947,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
             a.peer_n = nh;
             c->pushed_in_kernel = a.peer[0] || a.peer[1];
         }
+        if (Fch.size() > 1 && !v->kernel_acc) fail(SFSEG_ERR_STATE, "no accumulating kernel for this variant");
         for (size_t g = 0; g < Fch.size(); ++g) {
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->box_w, v->box_h);
             a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v->tx, v->slab_h);
@@ -1008,7 +969,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                 c->ev.push_back(e1);
             }
         }
-        return;
+        return false;
     }
     // generic multi-pass path (radii beyond the fused instantiations)
     sfk::Taps tp;
@@ -1044,6 +1005,7 @@ void launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
     sfk::k_partials<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, c->stream>>>(
         c->out_vol(out), c->part, c->frame_max, c->nbands(), c->nhalves(), 0);
     launched(c->stream, "k_partials");
+    return false;
 }
 
 void frame_sums(sfseg_ctx* c) {
@@ -1111,6 +1073,7 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
         set_state(c, c->st, s);
         ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
         c->cur = -1;
+        c->cur_u = false;
     }
     for (auto e : c->ev) cudaEventDestroy(e);
     c->ev.clear();
@@ -1120,7 +1083,11 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
     for (int it = first; it <= last; ++it) {
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
-        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->Fw, p->arith == SFSEG_ARITH_FAST);
+        // U_{k+1} = S^p y_{k+1} replaces y_{k+1} when the next iteration of
+        // this solve only normalises; the last one leaves y for the caller
+        const bool wu = it < last && it < p->binarize_start;
+        c->cur_u = launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->Fw,
+                               p->arith == SFSEG_ARITH_FAST, c->cur >= 0 && c->cur_u, wu);
         const int mode_next = it >= p->binarize_start ? 2 : 1;
         finalize(c, c->st, c->norms, it - first, mode_next, lambda_for(p, it), p->threshold_frac);
         c->cur = dst;
@@ -1327,6 +1294,7 @@ void load_impl(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, cons
     c->guard_applied = false;
     c->sp_p = NAN;
     c->cur = -1;
+    c->cur_u = false;
     c->has_x0 = x0 != nullptr;
     if (x0 && !c->x0) c->x0 = dalloc_vol(c);
     if (mem == SFSEG_MEM_HOST && c->P != c->W) {
@@ -1436,6 +1404,7 @@ void load_files_impl(sfseg_ctx* c, const char* unary, const char* const* pairwis
     c->guard_applied = false;
     c->sp_p = NAN;
     c->cur = -1;
+    c->cur_u = false;
     c->resident = false;
     stream_sfsv(c, files[0], unary, c->S);
     for (int i = 0; i < C; ++i) stream_sfsv(c, files[1 + i], pairwise[i], c->F[i]);
@@ -1460,6 +1429,7 @@ void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
     c->Fw = c->F;
     c->sp_p = NAN;
     c->cur = -1;
+    c->cur_u = false;
     c->has_x0 = false;
     c->resident = false;  // stateless operators reuse the resident buffers
     c->q_for.clear();     // the channel buffers get new contents: Q is stale
@@ -1850,6 +1820,40 @@ int sfseg_ctx_destroy(sfseg_ctx* c) {
         if (c->cstream) cudaStreamDestroy(c->cstream);
         cudaStreamDestroy(c->stream);
         delete c;
+    });
+}
+
+int sfseg_probe_fp32_peak(int device, double* tflops) {
+    return guarded([&] {
+        if (!tflops) fail(SFSEG_ERR_PARAMETER, "null argument");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        int sms = 0;
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attribute");
+        float* out = nullptr;
+        ck(cudaMalloc(&out, 1024 * sizeof(float)), "cudaMalloc");
+        cudaStream_t s;
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        const int blocks = sms * 4, threads = 512, iters = 1 << 14;
+        double best = 0.0;
+        for (int rep = 0; rep < 4; ++rep) {
+            cudaEventRecord(e0, s);
+            sfk::k_fma_probe<<<blocks, threads, 0, s>>>(out, 1.0001f, iters);
+            cudaEventRecord(e1, s);
+            ck(cudaEventSynchronize(e1), "probe");
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double flops = double(blocks) * threads * iters * 8 * 2 * 2;
+            if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        }
+        ck(cudaGetLastError(), "k_fma_probe");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(s);
+        cudaFree(out);
+        *tflops = best;
     });
 }
 
@@ -2244,6 +2248,7 @@ int sfseg_shard_load(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C
         c->guard_applied = false;
         c->sp_p = NAN;
         c->cur = -1;
+        c->cur_u = false;
         upload(c, c->S, S, mem);
         for (int i = 0; i < C; ++i) upload(c, c->F[i], F[i], mem);
         validate_vol(c, c->S, true, "unary");
@@ -2277,12 +2282,17 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
             s.mode = 0;
             set_state(c, c->st, s);
             c->cur = -1;
+            c->cur_u = false;
         }
         ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
         c->peer_push_dst = dst;
-        launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST);
+        // the same U_{k+1} rule as solve_impl, identical on every rank (the
+        // halo frames pushed below are then U as well)
+        const bool wu = iter < p->iterations && iter < p->binarize_start;
+        c->cur_u = launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, p->arith == SFSEG_ARITH_FAST,
+                               c->cur >= 0 && c->cur_u, wu);
         c->peer_push_dst = -1;
         const size_t fr = static_cast<size_t>(c->H) * c->P;  // floats per pitched frame
         // peer-memory halo push: my first / last rt output frames straight into

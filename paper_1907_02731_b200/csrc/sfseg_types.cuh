@@ -48,7 +48,7 @@ struct FusedArgs {
     float2 tpair_y[kMaxTapsXY + 1];
     float inv_alpha;
     float c_inv_alpha;  // C / alpha (fused_mc.cuh HEAD launch)
-    float* u_out;       // u = S^p x at the output points (fused_mc.cuh HEAD launch writes it)
+    int write_u;        // fused_mc.cuh last launch: store U_{k+1} = S^p y_{k+1} instead of y_{k+1}
     // time-sharded solve with peer-memory halos (fused_rs.cuh, last group):
     // output planes [out_t0, out_t0 + peer_n) also go to peer[0] (rank-1's
     // iterate buffer, frame origin peer_t0[0]) and [out_t1 - peer_n, out_t1)
