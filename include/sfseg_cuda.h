@@ -234,6 +234,14 @@ int sfseg_step_channel(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_
 int sfseg_normalize_l2(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
                        const float* x, float* out, double* norm, int32_t mem);
 
+/* scale_channel_into_unit_range (engine.cpp:228-243) on the device: if v
+ * leaves [0,1], out = (v - lo) / (hi - lo) (IEEE division), a constant
+ * channel becomes clamp(lo, 0, 1); otherwise out = v bit for bit. The guard
+ * run() applies to the pairwise channels when allow_negative_affinity is off
+ * (the drop-in's FrameTransform path needs it on host slices). */
+int sfseg_unit_range(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
+                     const float* v, float* out, int32_t mem);
+
 /* project_binary (engine.cpp:185-205). */
 int sfseg_project_binary(sfseg_ctx* ctx, uint32_t frames, uint32_t height, uint32_t width,
                          const float* x, int32_t iter, const sfseg_params* p, float* out,
@@ -380,6 +388,26 @@ int sfseg_affinity_power_iteration(sfseg_ctx* ctx, uint32_t frames, uint32_t hei
  * (CUDA failure). */
 int sfseg_synth_generate_device(const sfseg_synth_spec* spec, float* S, float* const* F,
                                 uint8_t* mask_out, void* stream);
+
+/* ---- in-process multi-GPU solve (SFSEG_NUM_GPUS in the C++ drop-in) ------
+ * run() over time shards on several devices of ONE process:
+ * shard i owns a contiguous frame range plus rt halo frames; every iteration
+ * each shard runs the fused step, stores its rt edge planes straight into
+ * its neighbours' halo frames (peer memory over NVLink) and publishes its
+ * per-frame sums and maxima; every shard then gathers all of them (peer
+ * copies, ordered by events, no host synchronisation) and derives the same
+ * frame-ordered norm. Results are bit-identical to one context for any
+ * shard count. devices may repeat (several shards on one GPU, for tests);
+ * NULL means 0..n-1. */
+typedef struct sfseg_multi sfseg_multi;
+int sfseg_multi_create(int32_t n, const int32_t* devices, sfseg_multi** out);
+int sfseg_multi_destroy(sfseg_multi* m);
+int sfseg_multi_size(const sfseg_multi* m);
+/* sfseg_run over the shards (records may be NULL). */
+int sfseg_multi_run(sfseg_multi* m, uint32_t frames, uint32_t height, uint32_t width,
+                    int32_t channels, const float* unary, const float* const* pairwise,
+                    const float* x0, const sfseg_params* p, float* soft, uint8_t* mask,
+                    sfseg_iter_record* records, int32_t mem);
 
 #ifdef __cplusplus
 }

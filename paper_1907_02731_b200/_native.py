@@ -176,6 +176,12 @@ _SIGS = {
     "sfseg_metrics": (C.c_int, [_P, _P, _P, C.c_double, C.POINTER(C.c_double),
                                 C.POINTER(C.c_double), _I32]),
     "sfseg_probe_fp32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "sfseg_unit_range": (C.c_int, [_P, _U32, _U32, _U32, _P, _P, _I32]),
+    "sfseg_multi_create": (C.c_int, [C.c_int32, _P, C.POINTER(_P)]),
+    "sfseg_multi_destroy": (C.c_int, [_P]),
+    "sfseg_multi_size": (C.c_int, [_P]),
+    "sfseg_multi_run": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, C.POINTER(Params), _P, _P,
+                                  _P, _I32]),
     "sfseg_run": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, C.POINTER(Params), _P, _P,
                             C.POINTER(IterRecord), _I32]),
     "sfseg_step": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, C.POINTER(Params), _P, _I32]),

@@ -194,7 +194,6 @@ struct FusedVariant {
     void (*kernel_acc)(FusedArgs);  // later channel groups (y += terms); may equal kernel
     int box_w, box_h;
     int slab_h = 8;  // rows of the recombination-operand / output TMA boxes
-    int ctas_per_sm = 1;  // persistent grid = ctas_per_sm x SMs
     bool rs = false;      // fused_rs.cuh (stores the sharded solve's edge planes to the peers)
     void (*kernel_peer)(FusedArgs) = nullptr;  // rs: single-group step + peer edge stores
 };
@@ -223,23 +222,14 @@ FusedVariant variant_ws() {
     return v;
 }
 
-#ifndef SFK_RS_NWA
-#define SFK_RS_NWA 8
-#endif
 #ifndef SFK_RS_STAGES
 #define SFK_RS_STAGES 3
 #endif
-#ifndef SFK_RS_TY
-#define SFK_RS_TY 64
-#endif
-#ifndef SFK_RS_BR
-#define SFK_RS_BR 8
-#endif
-// FAST: products formed in registers inside the x-pass (fused_rs.cuh)
-template <int RT, int R, int ST = SFK_RS_STAGES, bool TMR = (SFK_RS_TMR != 0), int NWA = SFK_RS_NWA,
-          int TY = SFK_RS_TY, int BR = SFK_RS_BR>
+// FAST, one channel: products formed in registers inside the x-pass, u read
+// as U = S^p x (fused_rs.cuh)
+template <int RT, int R, int ST = SFK_RS_STAGES, bool TMR = false>
 FusedVariant variant_rs() {
-    using G = sfk::RsGeom<RT, R, NWA, ST, TY, BR, TMR>;
+    using G = sfk::RsGeom<RT, R, ST, TMR>;
     FusedVariant v;
     v.rt = RT;
     v.r = R;
@@ -248,22 +238,21 @@ FusedVariant variant_rs() {
     v.fma = true;
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.slab_h = (SFK_RS_WIDE && !TMR) ? TY : 8;
-    v.ctas_per_sm = SFK_RS_CPS;
+    v.slab_h = TMR ? 8 : G::TY;  // TMEM-ring variants: per-warp slabs; else CTA-wide tiles
     v.rs = true;
-    v.kernel = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false>;
+    v.kernel = sfk::fused_step_rs<RT, R, ST, TMR>;
     v.kernel_acc = nullptr;  // FAST with C > 1 runs fused_mc.cuh (every rs radius has an mc variant)
-    v.kernel_peer = sfk::fused_step_rs<RT, R, NWA, ST, TY, BR, TMR, false, true>;
+    v.kernel_peer = sfk::fused_step_rs<RT, R, ST, TMR, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
 }
 
-// radii beyond (2, 5) (BASELINE c2: 3,7,7; c4: 4,10,10): 2 TMA stages and the
-// t-pass ring in tensor memory (a 7- or 9-plane register ring does not fit)
+// radii beyond (2, 5) (BASELINE c2: 3,7,7; c4: 4,10,10): the t-pass ring in
+// tensor memory (a 7- or 9-plane register ring does not fit)
 #define SFK_VARIANTS_RS()                                                                  \
     variant_rs<1, 2>(), variant_rs<1, 3>(), variant_rs<2, 4>(), variant_rs<2, 5>(),       \
-        variant_rs<3, 7, 2, true, 8, 64, 8>(), variant_rs<4, 10, 2, true, 8, 64, 8>()
+        variant_rs<3, 7, 2, true>(), variant_rs<4, 10, 2, true>()
 
 // FAST, C > 1: (C + 2)-field launches (fused_mc.cuh): a HEAD (u, Q u, f_1 u)
 // and TAILs of one or two channels (f_a u [, f_b u])
@@ -488,6 +477,8 @@ struct sfseg_ctx {
     sfseg_timing last_timing{};
     std::vector<cudaEvent_t> ev;
     std::mutex mu;
+    sfseg_ctx* scratch = nullptr;  // stateless operators (scratch_ctx)
+    std::mutex scratch_mu;
 
     size_t vol_elems() const { return static_cast<size_t>(T) * H * P; }
     Vol vol(float* p) const { return Vol{p, T, H, W, P}; }
@@ -563,10 +554,21 @@ void release_problem(sfseg_ctx* c) {
     c->guard_applied = false;
 }
 
+// VolumeShape::validate (volume.cpp:39-52) plus this library's own limits:
+// each axis, the pitched volume size (overflow-checked: the product of three
+// 32-bit extents does not fit 64 bits) and the per-frame reduction blocks
+// (an int in the kernels)
 void check_shape(uint32_t T, uint32_t H, uint32_t W) {
     if (T == 0 || H == 0 || W == 0) fail(SFSEG_ERR_VALIDATION, "volume shape has an empty axis");
     if (T > (1u << 30) || H > (1u << 20) || W > (1u << 20))
         fail(SFSEG_ERR_CAPACITY, "volume shape exceeds the supported extent");
+    const unsigned __int128 bytes = static_cast<unsigned __int128>(T) * H *
+                                    ((static_cast<uint64_t>(W) + 31) / 32 * 32) * sizeof(float);
+    if (bytes > (static_cast<unsigned __int128>(1) << 40))
+        fail(SFSEG_ERR_CAPACITY, "volume exceeds the supported size (1 TiB per field)");
+    const uint64_t blocks = (static_cast<uint64_t>(H) + 3) / 4 * ((static_cast<uint64_t>(W) + 31) / 32);
+    if (blocks > static_cast<uint64_t>(INT32_MAX) / 64)
+        fail(SFSEG_ERR_CAPACITY, "frame exceeds the supported size");
 }
 
 void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int Tg = -1,
@@ -891,7 +893,7 @@ bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         launch_step_mc(c, k, alpha, x_src, st, out, Fch, *mc, false, src_is_u, write_u);
         return write_u;
     }
-    if (src_is_u) fail(SFSEG_ERR_STATE, "iterate stored as S^p y for another step path");
+    if (src_is_u && !(v && v->rs)) fail(SFSEG_ERR_STATE, "iterate stored as S^p y for another step path");
     // EXACT beyond the warp-specialised instantiations (c2, c4 radii): the
     // per-channel EXACT launches of fused_mc.cuh
     const McVariant* mce = (!fma && !v) ? pick_mc(k.rt, k.ry, k.rx) : nullptr;
@@ -900,9 +902,21 @@ bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         return false;
     }
     if (v) {
+        // the FAST kernel (fused_rs.cuh) reads u = S^p x as a volume: the
+        // previous step's U store, or k_make_u; it stores U_{k+1} on request
+        const float* xin = x_src;
+        const bool wu = v->rs && write_u;
+        if (v->rs && !src_is_u) {
+            float* ub = tmp_vol(c, 0);
+            launch_pdl(sfk::k_make_u, aux_grid(c), sfk::kAuxThreads, 0, c->stream,
+                       c->vol(const_cast<float*>(x_src)), c->vol(c->sp), c->vol(ub), st);
+            launched(c->stream, "k_make_u");
+            xin = ub;
+        }
         FusedArgs a;
         std::memset(&a, 0, sizeof a);
-        a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
+        a.write_u = wu;
+        a.tm_x = make_tmap(xin, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
         a.tm_sp = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->box_w, v->box_h);
         a.tm_out = make_tmap(out, c->T, c->H, c->W, c->P, v->tx, v->slab_h);
         a.tm_spc = make_tmap(c->sp, c->T, c->H, c->W, c->P, v->tx, v->slab_h);
@@ -929,7 +943,7 @@ bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
         a.nbands = c->nbands();
         a.nhalves = c->nhalves();
         const int ntiles = a.tiles_x * a.tiles_y;
-        const int grid_n = c->num_sms * v->ctas_per_sm;
+        const int grid_n = c->num_sms;
         upload_schedule(c, ntiles, c->Tout(), grid_n);
         a.sched = c->sched_seg;
         a.sched_off = c->sched_off;
@@ -969,7 +983,7 @@ bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
                 c->ev.push_back(e1);
             }
         }
-        return false;
+        return wu;
     }
     // generic multi-pass path (radii beyond the fused instantiations)
     sfk::Taps tp;
@@ -1422,11 +1436,25 @@ void load_files_impl(sfseg_ctx* c, const char* unary, const char* const* pairwis
 }
 
 // stateless helpers: (re)use the resident buffers of a scratch problem
+// The stateless operators (sfseg_step, normalize_l2, ...) run on a scratch
+// context owned by the caller's context (same device, own stream and
+// buffers), so they can be called between or during the iterations of a
+// resident solve (an IterationObserver) without touching its problem.
+sfseg_ctx* scratch_ctx(sfseg_ctx* owner) {
+    std::lock_guard<std::mutex> lk(owner->scratch_mu);
+    if (!owner->scratch) {
+        sfseg_ctx* s = nullptr;
+        const int rc = sfseg_ctx_create(owner->device, &s);
+        if (rc != SFSEG_OK) fail(rc, sfseg_last_error());
+        owner->scratch = s;
+    }
+    return owner->scratch;
+}
+
 void stage_volume(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C) {
     check_shape(T, H, W);
     set_shape(c, T, H, W, C);
-    c->guard_applied = false;
-    c->Fw = c->F;
+    ensure_guard(c, false);  // drops guard copies of an earlier call (Fw = F)
     c->sp_p = NAN;
     c->cur = -1;
     c->cur_u = false;
@@ -1790,6 +1818,7 @@ int sfseg_ctx_create(int device, sfseg_ctx** out) {
 int sfseg_ctx_destroy(sfseg_ctx* c) {
     return guarded([&] {
         if (!c) return;
+        if (c->scratch) sfseg_ctx_destroy(c->scratch);
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
         release_problem(c);
@@ -1941,21 +1970,28 @@ int sfseg_solve_until(sfseg_ctx* c, const sfseg_params* p, int32_t first, int32_
     });
 }
 
+namespace {
+// caller holds c->mu and has selected the device
+void download_impl(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, int32_t mem) {
+    if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_download before sfseg_load");
+    float* x = tmp_vol(c, 0);
+    materialize(c, x);
+    if (soft && mem == SFSEG_MEM_HOST && c->P != c->W) {
+        download_pipelined(c, soft, x, frac, mask);
+    } else {
+        if (soft) download(c, soft, x, mem);
+        if (mask) mask_of(c, x, frac, mask, mem);
+    }
+    ck(cudaStreamSynchronize(c->stream), "download");
+}
+}  // namespace
+
 int sfseg_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, int32_t mem) {
     return guarded([&] {
         if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
         std::lock_guard<std::mutex> lk(c->mu);
-        if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_download before sfseg_load");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        float* x = tmp_vol(c, 0);
-        materialize(c, x);
-        if (soft && mem == SFSEG_MEM_HOST && c->P != c->W) {
-            download_pipelined(c, soft, x, frac, mask);
-        } else {
-            if (soft) download(c, soft, x, mem);
-            if (mask) mask_of(c, x, frac, mask, mem);
-        }
-        ck(cudaStreamSynchronize(c->stream), "download");
+        download_impl(c, frac, soft, mask, mem);
     });
 }
 
@@ -2013,29 +2049,29 @@ int sfseg_metrics(sfseg_ctx* c, const float* reference, const uint8_t* gt, doubl
 int sfseg_run(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
               const float* const* F, const float* x0, const sfseg_params* p, float* soft,
               uint8_t* mask, sfseg_iter_record* rec, int32_t mem) {
-    int rc = sfseg_params_validate(p);
-    if (rc) return rc;
-    // sfseg_load, with p known: S^p is computed under the DMA of the channels
-    rc = guarded([&] {
+    // load (S^p computed under the DMA of the channels, p being known),
+    // solve and download under ONE hold of the context lock: the call is
+    // atomic with respect to other users of the context
+    return guarded([&] {
         if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        validate_params(p);
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         load_impl(c, T, H, W, C, S, F, x0, mem, p->p);
+        solve_impl(c, p, 1, p->iterations, rec);
+        download_impl(c, p->final_threshold, soft, mask, mem);
     });
-    if (rc) return rc;
-    rc = sfseg_solve(c, p, 1, p->iterations, rec);
-    if (rc) return rc;
-    return sfseg_download(c, p->final_threshold, soft, mask, mem);
 }
 
-int sfseg_step(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* x,
+int sfseg_step(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* x,
                const float* S, const float* const* F, const sfseg_params* p, float* out,
                int32_t mem) {
     return guarded([&] {
-        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        if (!owner) fail(SFSEG_ERR_PARAMETER, "null ctx");
         validate_params(p);  // engine.cpp:143
         if (C < 1) fail(SFSEG_ERR_PARAMETER, "sfseg_step needs at least one pairwise channel");
         if (!x || !S || !F || !out) fail(SFSEG_ERR_PARAMETER, "null input");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         const HostKernel k = make_kernel(p->radii, p->sigmas);
@@ -2063,11 +2099,12 @@ int sfseg_step_channel(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const f
     return sfseg_step(c, T, H, W, 1, x, S, F, p, out, mem);
 }
 
-int sfseg_normalize_l2(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+int sfseg_normalize_l2(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* x,
                        float* out, double* norm, int32_t mem) {
     return guarded([&] {
-        if (!c) fail(SFSEG_ERR_PARAMETER, "null ctx");
+        if (!owner) fail(SFSEG_ERR_PARAMETER, "null ctx");
         if (!x) fail(SFSEG_ERR_PARAMETER, "null input");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         stage_volume(c, T, H, W, 1);
@@ -2089,10 +2126,26 @@ int sfseg_normalize_l2(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const f
     });
 }
 
-int sfseg_project_binary(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+int sfseg_unit_range(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* v,
+                     float* out, int32_t mem) {
+    return guarded([&] {
+        if (!owner || !v || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        stage_volume(c, T, H, W, 1);
+        upload(c, c->F[0], v, mem);
+        ensure_guard(c, true);  // k_minmax_* + k_unit_range (IEEE divide), engine.cpp:228-243
+        download(c, out, c->Fw[0], mem);
+        ck(cudaStreamSynchronize(c->stream), "unit_range");
+    });
+}
+
+int sfseg_project_binary(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* x,
                          int32_t iter, const sfseg_params* p, float* out, int32_t mem) {
     return guarded([&] {
-        if (!c || !p || !x || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!owner || !p || !x || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         stage_volume(c, T, H, W, 1);
@@ -2121,10 +2174,11 @@ int sfseg_project_binary(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const
     });
 }
 
-int sfseg_threshold_final(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* x,
+int sfseg_threshold_final(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* x,
                           double frac, uint8_t* mask, int32_t mem) {
     return guarded([&] {
-        if (!c || !x || !mask) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!owner || !x || !mask) fail(SFSEG_ERR_PARAMETER, "null argument");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         stage_volume(c, T, H, W, 1);
@@ -2135,11 +2189,12 @@ int sfseg_threshold_final(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, cons
     });
 }
 
-int sfseg_convolve_separable(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* v,
+int sfseg_convolve_separable(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* v,
                              const int32_t radii[3], const double sigmas[3], float* out,
                              int32_t mem) {
     return guarded([&] {
-        if (!c || !v || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!owner || !v || !out) fail(SFSEG_ERR_PARAMETER, "null argument");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         const HostKernel k = make_kernel(radii, sigmas);
@@ -2166,13 +2221,14 @@ int sfseg_convolve_separable(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, c
     });
 }
 
-int sfseg_convolve_separable_taps(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W,
+int sfseg_convolve_separable_taps(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W,
                                   const float* v, const int32_t radii[3], const double* tt,
                                   const double* ty, const double* tx, float* out, int32_t mem) {
     return guarded([&] {
-        if (!c || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!owner || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
         for (int i = 0; i < 3; ++i)
             if (radii[i] < 0 || radii[i] > 31) fail(SFSEG_ERR_CAPACITY, "kernel radius above 31");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         stage_volume(c, T, H, W, 1);
@@ -2197,13 +2253,14 @@ int sfseg_convolve_separable_taps(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t
     });
 }
 
-int sfseg_convolve_direct_taps(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, const float* v,
+int sfseg_convolve_direct_taps(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, const float* v,
                                const int32_t radii[3], const double* tt, const double* ty,
                                const double* tx, float* out, int32_t mem) {
     return guarded([&] {
-        if (!c || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!owner || !v || !out || !radii || !tt || !ty || !tx) fail(SFSEG_ERR_PARAMETER, "null argument");
         for (int i = 0; i < 3; ++i)
             if (radii[i] < 0 || radii[i] > 15) fail(SFSEG_ERR_CAPACITY, "direct kernel radius above 15");
+        sfseg_ctx* const c = scratch_ctx(owner);  // never the resident problem
         std::lock_guard<std::mutex> lk(c->mu);
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         stage_volume(c, T, H, W, 1);
@@ -2487,6 +2544,307 @@ int sfseg_shard_download(sfseg_ctx* c, double frac, float* soft, uint8_t* mask, 
             }
         }
         ck(cudaStreamSynchronize(c->stream), "shard download");
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// In-process multi-GPU solve (SFSEG_NUM_GPUS in the drop-in): time shards on
+// several devices of one process, every exchange device-side and ordered by
+// events; no per-iteration host synchronisation, no collective library.
+//   per iteration, shard i (its own device and stream):
+//     1. fused step over its frames; the rt edge planes of the new iterate go
+//        straight into the neighbours' halo frames (peer stores, in-kernel for
+//        the FAST single-channel kernel, else k_halo_push); per-frame sums
+//        and maxima of its frames (frame_sums); event done[i]
+//     2. waits for done[j] of every shard, copies their per-frame sums and
+//        maxima into its own frame-ordered arrays (peer copies), and runs the
+//        same frame-ordered finalize as a single context: every shard derives
+//        bit-identical norms and projection scalars
+//   The per-frame results are copied into one of two published sets by
+//   iteration parity, so a shard's step k+1 never overwrites what a slower
+//   shard still gathers.
+struct sfseg_multi {
+    std::vector<sfseg_ctx*> shards;
+    std::vector<int> t0, t1;
+    std::vector<double*> fsum[2];  // per shard: its frame sums, by iteration parity
+    std::vector<float*> fmax[2];
+    std::vector<double*> gsum;     // per shard: all Tg frame sums, frame order
+    std::vector<float*> gmax;
+    std::vector<cudaEvent_t> done;
+    int T = 0, halo = -1;
+    std::mutex mu;
+};
+
+namespace {
+
+void multi_free_buffers(sfseg_multi* m) {
+    for (size_t i = 0; i < m->shards.size(); ++i) {
+        cudaSetDevice(m->shards[i]->device);
+        for (int b = 0; b < 2; ++b) {
+            if (i < m->fsum[b].size() && m->fsum[b][i]) cudaFree(m->fsum[b][i]);
+            if (i < m->fmax[b].size() && m->fmax[b][i]) cudaFree(m->fmax[b][i]);
+        }
+        if (i < m->gsum.size() && m->gsum[i]) cudaFree(m->gsum[i]);
+        if (i < m->gmax.size() && m->gmax[i]) cudaFree(m->gmax[i]);
+    }
+    for (int b = 0; b < 2; ++b) {
+        m->fsum[b].clear();
+        m->fmax[b].clear();
+    }
+    m->gsum.clear();
+    m->gmax.clear();
+}
+
+// global unit-range guard (engine.cpp:254-259) across shards: min/max of each
+// channel over every shard's frames, then the same rescale on every shard
+void multi_guard(sfseg_multi* m, int C) {
+    for (int ch = 0; ch < C; ++ch) {
+        float lo = INFINITY, hi = -INFINITY;
+        for (sfseg_ctx* c : m->shards) {
+            ck(cudaSetDevice(c->device), "cudaSetDevice");
+            const int nb = aux_grid(c);
+            sfk::k_minmax_blocks<<<nb, sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->F[ch]), c->bminmax,
+                                                                        c->bminmax + nb);
+            sfk::k_minmax_final<<<1, sfk::kAuxThreads, 0, c->stream>>>(c->bminmax, c->bminmax + nb, nb,
+                                                                     c->scratch_f);
+            float lh[2];
+            ck(cudaMemcpyAsync(lh, c->scratch_f, sizeof lh, cudaMemcpyDeviceToHost, c->stream), "minmax");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            lo = std::min(lo, lh[0]);
+            hi = std::max(hi, lh[1]);
+        }
+        if (lo >= 0.0f && hi <= 1.0f) continue;  // bits untouched
+        const float lohi[2] = {lo, hi};
+        for (sfseg_ctx* c : m->shards) {
+            ck(cudaSetDevice(c->device), "cudaSetDevice");
+            ck(cudaMemcpyAsync(c->scratch_f, lohi, sizeof lohi, cudaMemcpyHostToDevice, c->stream), "lohi");
+            sfk::k_unit_range<<<aux_grid(c), sfk::kAuxThreads, 0, c->stream>>>(c->vol(c->F[ch]), c->scratch_f);
+            launched(c->stream, "k_unit_range");
+            ck(cudaStreamSynchronize(c->stream), "sync");  // lohi is a host stack array
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfseg_multi_create(int32_t n, const int32_t* devices, sfseg_multi** out) {
+    return guarded([&] {
+        if (!out || n < 1) fail(SFSEG_ERR_PARAMETER, "bad argument");
+        auto m = std::make_unique<sfseg_multi>();
+        for (int i = 0; i < n; ++i) {
+            sfseg_ctx* c = nullptr;
+            const int rc = sfseg_ctx_create(devices ? devices[i] : i, &c);
+            if (rc != SFSEG_OK) {
+                for (sfseg_ctx* d : m->shards) sfseg_ctx_destroy(d);
+                fail(rc, sfseg_last_error());
+            }
+            m->shards.push_back(c);
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            m->done.push_back(e);
+        }
+        // neighbours on other devices address each other's buffers directly
+        for (int i = 0; i + 1 < n; ++i) {
+            const int a = m->shards[i]->device, b = m->shards[i + 1]->device;
+            if (a == b) continue;
+            for (auto [x, y] : {std::pair<int, int>{a, b}, std::pair<int, int>{b, a}}) {
+                int can = 0;
+                ck(cudaDeviceCanAccessPeer(&can, x, y), "cudaDeviceCanAccessPeer");
+                if (!can) fail(SFSEG_ERR_CUDA, "devices without peer access");
+                ck(cudaSetDevice(x), "cudaSetDevice");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(y, 0);
+                if (e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+                cudaGetLastError();
+            }
+        }
+        *out = m.release();
+    });
+}
+
+int sfseg_multi_destroy(sfseg_multi* m) {
+    return guarded([&] {
+        if (!m) return;
+        multi_free_buffers(m);
+        for (size_t i = 0; i < m->shards.size(); ++i) {
+            cudaSetDevice(m->shards[i]->device);
+            cudaEventDestroy(m->done[i]);
+            sfseg_ctx_destroy(m->shards[i]);
+        }
+        delete m;
+    });
+}
+
+int sfseg_multi_size(const sfseg_multi* m) { return m ? static_cast<int>(m->shards.size()) : 0; }
+
+int sfseg_multi_run(sfseg_multi* m, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* S,
+                    const float* const* F, const float* x0, const sfseg_params* p, float* soft,
+                    uint8_t* mask, sfseg_iter_record* rec, int32_t mem) {
+    return guarded([&] {
+        if (!m || !S || !F || !p) fail(SFSEG_ERR_PARAMETER, "null argument");
+        validate_params(p);
+        check_shape(T, H, W);
+        if (C < 1) fail(SFSEG_ERR_VALIDATION, "feature set needs at least one pairwise channel");
+        std::lock_guard<std::mutex> lk(m->mu);
+        const int halo = p->radii[0];
+        // shards of at least max(halo, 1) frames: a halo comes from one neighbour
+        const int n = std::max(1, std::min<int>(static_cast<int>(m->shards.size()),
+                                                static_cast<int>(T) / std::max(1, halo)));
+        const size_t frame = static_cast<size_t>(H) * W;
+        m->t0.assign(n, 0);
+        m->t1.assign(n, 0);
+        for (int i = 0; i < n; ++i) {  // balanced contiguous frames (sharding.py shard_range)
+            const int base = static_cast<int>(T) / n, rem = static_cast<int>(T) % n;
+            m->t0[i] = i * base + std::min(i, rem);
+            m->t1[i] = m->t0[i] + base + (i < rem ? 1 : 0);
+        }
+        multi_free_buffers(m);
+        for (int i = 0; i < n; ++i) {
+            sfseg_ctx* c = m->shards[i];
+            const int b0 = std::max(0, m->t0[i] - halo);
+            std::vector<const float*> Fi(C);
+            for (int ch = 0; ch < C; ++ch) Fi[ch] = F[ch] + b0 * frame;
+            const int rc = sfseg_shard_load(c, T, H, W, C, m->t0[i], m->t1[i], halo, S + b0 * frame,
+                                            Fi.data(), x0 ? x0 + b0 * frame : nullptr, mem);
+            if (rc != SFSEG_OK) fail(rc, sfseg_last_error());
+        }
+        std::vector<sfseg_ctx*> sh(m->shards.begin(), m->shards.begin() + n);
+        if (!p->allow_negative_affinity) multi_guard(m, C);
+        for (int i = 0; i < n; ++i) {
+            sfseg_ctx* c = sh[i];
+            ck(cudaSetDevice(c->device), "cudaSetDevice");
+            for (int b = 0; b < 2; ++b) {
+                double* s2 = nullptr;
+                float* m2 = nullptr;
+                ck(cudaMalloc(&s2, c->Tout() * sizeof(double)), "malloc");
+                ck(cudaMalloc(&m2, c->Tout() * sizeof(float)), "malloc");
+                m->fsum[b].push_back(s2);
+                m->fmax[b].push_back(m2);
+            }
+            double* gs = nullptr;
+            float* gm = nullptr;
+            ck(cudaMalloc(&gs, T * sizeof(double)), "malloc");
+            ck(cudaMalloc(&gm, T * sizeof(float)), "malloc");
+            m->gsum.push_back(gs);
+            m->gmax.push_back(gm);
+            // neighbours' iterate buffers (same process: plain pointers)
+            drop_peers(c);
+            for (int side = 0; side < 2; ++side) {
+                const int j = side == 0 ? i - 1 : i + 1;
+                if (j < 0 || j >= n) continue;
+                for (int b = 0; b < 2; ++b) c->peer_y[side][b] = sh[j]->y[b];
+                c->peer_buf_t0[side] = sh[j]->buf_t0;
+                c->peer_ipc[side] = false;
+            }
+            if (c->norms_cap < p->iterations) {
+                if (c->norms) cudaFree(c->norms);
+                c->norms = nullptr;
+                ck(cudaMalloc(&c->norms, p->iterations * sizeof(double)), "cudaMalloc norms");
+                c->norms_cap = p->iterations;
+            }
+            ensure_sp(c, p->p);
+            IterState s0{};
+            set_state(c, c->st, s0);
+            c->cur = -1;
+            c->cur_u = false;
+        }
+        const HostKernel k = make_kernel(p->radii, p->sigmas);
+        const bool fast = p->arith == SFSEG_ARITH_FAST;
+        // per-iteration times on shard 0's stream (its finalize waits for every shard)
+        ck(cudaSetDevice(sh[0]->device), "cudaSetDevice");
+        std::vector<cudaEvent_t> iev(p->iterations + 1);
+        for (auto& e : iev) ck(cudaEventCreate(&e), "event");
+        ck(cudaEventRecord(iev[0], sh[0]->stream), "event");
+        for (int it = 1; it <= p->iterations; ++it) {
+            const int par = it & 1;
+            const bool wu = it < p->iterations && it < p->binarize_start;
+            bool wrote_u = false;
+            for (int i = 0; i < n; ++i) {
+                sfseg_ctx* c = sh[i];
+                ck(cudaSetDevice(c->device), "cudaSetDevice");
+                ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
+                const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
+                const int dst = c->cur < 0 ? 0 : 1 - c->cur;
+                c->peer_push_dst = dst;
+                wrote_u = launch_step(c, k, p->alpha, src, c->st, c->y[dst], c->F, fast,
+                                      c->cur >= 0 && c->cur_u, wu);
+                c->peer_push_dst = -1;
+                const size_t fr = static_cast<size_t>(c->H) * c->P;
+                const int nh = std::min(c->halo, c->Tout());
+                for (int side = 0; side < 2 && !c->pushed_in_kernel; ++side) {
+                    float* peer = c->peer_y[side][dst];
+                    if (!peer || nh == 0) continue;
+                    const int g0 = side == 0 ? c->out_t0 : c->out_t1 - nh;
+                    sfk::k_halo_push<<<c->num_sms * 2, 256, 0, c->stream>>>(
+                        reinterpret_cast<const float4*>(c->y[dst] + static_cast<size_t>(g0 - c->buf_t0) * fr),
+                        reinterpret_cast<float4*>(peer + static_cast<size_t>(g0 - c->peer_buf_t0[side]) * fr),
+                        static_cast<size_t>(nh) * fr / 4);
+                    launched(c->stream, "k_halo_push");
+                }
+                frame_sums(c);
+                ck(cudaMemcpyAsync(m->fsum[par][i], c->frame_sum, c->Tout() * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream), "publish sums");
+                ck(cudaMemcpyAsync(m->fmax[par][i], c->frame_max, c->Tout() * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, c->stream), "publish max");
+                c->cur = dst;
+                ck(cudaEventRecord(m->done[i], c->stream), "event");
+            }
+            const int mode_next = it >= p->binarize_start ? 2 : 1;
+            for (int i = 0; i < n; ++i) {
+                sfseg_ctx* c = sh[i];
+                ck(cudaSetDevice(c->device), "cudaSetDevice");
+                c->cur_u = wrote_u;
+                for (int j = 0; j < n; ++j) {
+                    ck(cudaStreamWaitEvent(c->stream, m->done[j], 0), "wait");
+                    const int tj = m->t1[j] - m->t0[j];
+                    ck(cudaMemcpyAsync(m->gsum[i] + m->t0[j], m->fsum[par][j], tj * sizeof(double),
+                                       cudaMemcpyDefault, c->stream), "gather sums");
+                    ck(cudaMemcpyAsync(m->gmax[i] + m->t0[j], m->fmax[par][j], tj * sizeof(float),
+                                       cudaMemcpyDefault, c->stream), "gather max");
+                }
+                sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
+                    m->gsum[i], m->gmax[i], static_cast<int>(T), c->st, c->norms, it - 1, mode_next,
+                    lambda_for(p, it), p->threshold_frac);
+                launched(c->stream, "k_finalize_total");
+                if (i == 0) ck(cudaEventRecord(iev[it], c->stream), "event");
+            }
+        }
+        // download: each shard's own frames; the mask cut comes from the
+        // shared (identical) projection state
+        std::vector<double> norms(p->iterations);
+        for (int i = 0; i < n; ++i) {
+            sfseg_ctx* c = sh[i];
+            ck(cudaSetDevice(c->device), "cudaSetDevice");
+            if (i == 0)
+                ck(cudaMemcpyAsync(norms.data(), c->norms, p->iterations * sizeof(double),
+                                   cudaMemcpyDeviceToHost, c->stream), "norms");
+            ck(cudaStreamSynchronize(c->stream), "solve");
+        }
+        for (double v : norms)
+            if (v == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+        for (int i = 0; i < n; ++i) {
+            sfseg_ctx* c = sh[i];
+            const size_t off = static_cast<size_t>(m->t0[i]) * frame;
+            const int rc = sfseg_shard_download(c, p->final_threshold, soft ? soft + off : nullptr,
+                                                mask ? mask + off : nullptr, mem);
+            if (rc != SFSEG_OK) fail(rc, sfseg_last_error());
+        }
+        for (int i = 0; i < p->iterations; ++i) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, iev[i], iev[i + 1]);
+            if (rec) {
+                rec[i].iter = i + 1;
+                rec[i].l2_norm_pre_normalize = norms[i];
+                rec[i].angle_deg = NAN;
+                rec[i].iou = NAN;
+                rec[i].wall_time_s = ms * 1e-3;
+            }
+        }
+        ck(cudaSetDevice(sh[0]->device), "cudaSetDevice");
+        for (auto e : iev) cudaEventDestroy(e);
     });
 }
 

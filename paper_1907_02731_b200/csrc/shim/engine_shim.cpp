@@ -9,8 +9,21 @@
 //
 // Environment: SFSEG_DEVICE (default 0) picks the GPU; SFSEG_ARITH=fast
 // selects fused multiply-adds (default "exact": the reference's rounding).
+// SFSEG_NUM_GPUS=N (SfsegConfig has no device field and stays unchanged)
+// runs run() time-sharded over N GPUs of this process (sfseg_multi_run:
+// peer-memory halos, bit-identical results); SFSEG_MULTI_DEVICES=0,0,1,...
+// maps the shards to devices explicitly (tests put several on one GPU).
 // SfsegConfig::threads is accepted and ignored, as the reference guarantees
 // thread-count-invariant results (README.md:174-189).
+//
+// Threading: the reference's functions are pure and
+// reentrant. Here every call leases a library context from a pool for its
+// whole duration (load, solve and download of run() included), so calls
+// from several host threads run side by side on their own contexts, and an
+// IterationObserver or FrameTransform that calls back into the engine gets
+// a context of its own. Idle contexts keep their device buffers for the next
+// call of the same shape.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -28,8 +41,10 @@
 
 namespace {
 
-std::mutex g_mu;
-sfseg_ctx* g_ctx = nullptr;
+int device_of_env() {
+    const char* d = std::getenv("SFSEG_DEVICE");
+    return d ? std::atoi(d) : 0;
+}
 
 [[noreturn]] void rethrow(int rc) {
     const std::string msg = sfseg_last_error();
@@ -47,14 +62,84 @@ void check(int rc) {
     if (rc != SFSEG_OK) rethrow(rc);
 }
 
-sfseg_ctx* ctx() {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_ctx) {
-        const char* d = std::getenv("SFSEG_DEVICE");
-        check(sfseg_ctx_create(d ? std::atoi(d) : 0, &g_ctx));
+// Pool of library contexts; a Lease holds one exclusively for one call.
+class Pool {
+  public:
+    sfseg_ctx* take() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (!idle_.empty()) {
+                sfseg_ctx* c = idle_.back();  // most recently used: warm buffers
+                idle_.pop_back();
+                return c;
+            }
+        }
+        sfseg_ctx* c = nullptr;
+        check(sfseg_ctx_create(device_of_env(), &c));
+        return c;
     }
-    return g_ctx;
+    void give(sfseg_ctx* c) {
+        std::lock_guard<std::mutex> lk(mu_);
+        idle_.push_back(c);
+    }
+
+  private:
+    std::mutex mu_;
+    std::vector<sfseg_ctx*> idle_;  // released with the process
+};
+
+Pool& pool() {
+    static Pool* p = new Pool();  // never destroyed: callers may run at exit
+    return *p;
 }
+
+// The in-process multi-GPU solver of SFSEG_NUM_GPUS > 1 (one per process;
+// run() calls take turns on it).
+struct Multi {
+    std::mutex mu;
+    sfseg_multi* m = nullptr;
+};
+
+int num_gpus_of_env() {
+    const char* n = std::getenv("SFSEG_NUM_GPUS");
+    return n ? std::max(1, std::atoi(n)) : 1;
+}
+
+Multi* multi() {
+    static Multi* g = [] {
+        auto* x = new Multi();
+        const int n = num_gpus_of_env();
+        if (n > 1) {
+            std::vector<int32_t> dev;
+            if (const char* d = std::getenv("SFSEG_MULTI_DEVICES")) {
+                std::string s(d);
+                size_t pos = 0;
+                while (pos <= s.size() && static_cast<int>(dev.size()) < n) {
+                    const size_t c = s.find(',', pos);
+                    dev.push_back(std::atoi(s.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str()));
+                    if (c == std::string::npos) break;
+                    pos = c + 1;
+                }
+            }
+            while (static_cast<int>(dev.size()) < n) dev.push_back(static_cast<int32_t>(dev.size()));
+            check(sfseg_multi_create(n, dev.data(), &x->m));
+        }
+        return x;
+    }();
+    return g;
+}
+
+class Lease {
+  public:
+    Lease() : c_(pool().take()) {}
+    ~Lease() { pool().give(c_); }
+    Lease(const Lease&) = delete;
+    Lease& operator=(const Lease&) = delete;
+    sfseg_ctx* get() const { return c_; }
+
+  private:
+    sfseg_ctx* c_;
+};
 
 int arith() {
     const char* a = std::getenv("SFSEG_ARITH");
@@ -86,33 +171,15 @@ void same_shape(const sfseg::FeatureVolume& a, const sfseg::FeatureVolume& b, co
     if (!(a.shape() == b.shape())) throw sfseg::ShapeError(std::string("shape mismatch: ") + what);
 }
 
-sfseg::FeatureVolume slice_frames(const sfseg::FeatureVolume& v, std::uint32_t t0,
-                                  std::uint32_t t1) {
-    const auto& s = v.shape();
-    const std::size_t plane = static_cast<std::size_t>(s.height) * s.width;
-    sfseg::FeatureVolume out(sfseg::VolumeShape{t1 - t0 + 1, s.height, s.width}, v.role());
-    std::memcpy(out.data(), v.data() + static_cast<std::size_t>(t0) * plane,
-                sizeof(float) * out.size());
-    return out;
-}
-
-// unit-range guard on a host copy (engine.cpp:228-243); only the FrameTransform
-// path needs host-side channels, the resident solve applies it on the GPU
-void unit_range_host(sfseg::FeatureVolume& f) {
-    float lo = f.data()[0], hi = f.data()[0];
-    for (float v : f.values()) {
-        lo = std::min(lo, v);
-        hi = std::max(hi, v);
-    }
-    if (lo >= 0.0f && hi <= 1.0f) return;
-    float* p = f.data();
-    if (hi > lo) {
-        const float span = hi - lo;
-        for (std::size_t i = 0; i < f.size(); ++i) p[i] = (p[i] - lo) / span;
-    } else {
-        const float c = std::clamp(lo, 0.0f, 1.0f);
-        for (std::size_t i = 0; i < f.size(); ++i) p[i] = c;
-    }
+// frames [t0, t1] (inclusive) of v as a volume of their own: the window a
+// FrameTransform sees (engine.cpp:295-303)
+sfseg::FeatureVolume window_of(const sfseg::FeatureVolume& v, std::uint32_t t0, std::uint32_t t1) {
+    const auto& sh = v.shape();
+    const std::size_t frame = static_cast<std::size_t>(sh.height) * sh.width;
+    sfseg::FeatureVolume w(sfseg::VolumeShape{t1 - t0 + 1, sh.height, sh.width}, v.role());
+    const float* from = v.data() + frame * t0;
+    std::copy(from, from + w.size(), w.data());
+    return w;
 }
 
 }  // namespace
@@ -134,7 +201,8 @@ FeatureVolume sfseg_step_channel(const FeatureVolume& x, const FeatureVolume& s,
     const sfseg_params p = to_params(cfg);
     const auto& sh = x.shape();
     FeatureVolume out(sh, VolumeRole::solution);
-    check(sfseg_step_channel(ctx(), sh.frames, sh.height, sh.width, x.data(), s.data(), f.data(),
+    Lease lease;
+    check(sfseg_step_channel(lease.get(), sh.frames, sh.height, sh.width, x.data(), s.data(), f.data(),
                              &p, out.data(), SFSEG_MEM_HOST));
     return out;
 }
@@ -151,7 +219,8 @@ FeatureVolume sfseg_step(const FeatureVolume& x, const FeatureSet& features,
     std::vector<const float*> F;
     for (const auto& f : features.pairwise) F.push_back(f.data());
     FeatureVolume out(sh, VolumeRole::solution);
-    check(sfseg_step(ctx(), sh.frames, sh.height, sh.width, static_cast<int32_t>(F.size()),
+    Lease lease;
+    check(sfseg_step(lease.get(), sh.frames, sh.height, sh.width, static_cast<int32_t>(F.size()),
                      x.data(), features.unary.data(), F.data(), &p, out.data(), SFSEG_MEM_HOST));
     return out;
 }
@@ -160,7 +229,8 @@ std::pair<FeatureVolume, double> normalize_l2(const FeatureVolume& x) {
     const auto& sh = x.shape();
     FeatureVolume out(sh, x.role());
     double norm = 0.0;
-    check(sfseg_normalize_l2(ctx(), sh.frames, sh.height, sh.width, x.data(), out.data(), &norm,
+    Lease lease;
+    check(sfseg_normalize_l2(lease.get(), sh.frames, sh.height, sh.width, x.data(), out.data(), &norm,
                              SFSEG_MEM_HOST));
     return {std::move(out), norm};
 }
@@ -170,7 +240,8 @@ FeatureVolume project_binary(const FeatureVolume& x, int iter, const SfsegConfig
     const sfseg_params p = to_params(cfg);
     const auto& sh = x.shape();
     FeatureVolume out(sh, x.role());
-    check(sfseg_project_binary(ctx(), sh.frames, sh.height, sh.width, x.data(), iter, &p,
+    Lease lease;
+    check(sfseg_project_binary(lease.get(), sh.frames, sh.height, sh.width, x.data(), iter, &p,
                                out.data(), SFSEG_MEM_HOST));
     return out;
 }
@@ -180,59 +251,64 @@ BinaryMask threshold_final(const FeatureVolume& x, double frac) {
     BinaryMask m;
     m.shape = sh;
     m.values.resize(x.size());
-    check(sfseg_threshold_final(ctx(), sh.frames, sh.height, sh.width, x.data(), frac,
+    Lease lease;
+    check(sfseg_threshold_final(lease.get(), sh.frames, sh.height, sh.width, x.data(), frac,
                                 m.values.data(), SFSEG_MEM_HOST));
     return m;
 }
 
 namespace {
 
-// run() with a FrameTransform: the per-frame windowed sweep of
-// engine.cpp:287-325 with the hook on host slices and every step on the GPU
+// run() with a FrameTransform (engine.cpp:284-347): the hook needs the
+// reference's per-frame Jacobi windows on the host, so each frame's window
+// of x, S and F goes through the hook and then through sfseg_step on the
+// GPU; the frame's own plane of the result is kept. The unit-range guard of
+// the pairwise channels (engine.cpp:254-259) runs on the device.
 RunResult run_windowed(const FeatureSet& features, const SfsegConfig& cfg,
                        const FeatureVolume* x0, const FeatureVolume* reference,
                        const BinaryMask* ground_truth, const FrameTransform& transform,
                        const IterationObserver& observer) {
-    const VolumeShape shape = features.shape();
-    FeatureSet work = features;
-    if (!cfg.allow_negative_affinity)
-        for (auto& f : work.pairwise) unit_range_host(f);
-    FeatureVolume x = x0 ? *x0 : work.unary;
+    const VolumeShape sh = features.shape();
+    FeatureSet guarded_set = features;
+    if (!cfg.allow_negative_affinity) {
+        Lease lease;
+        for (auto& f : guarded_set.pairwise)
+            check(sfseg_unit_range(lease.get(), sh.frames, sh.height, sh.width, f.data(), f.data(),
+                                   SFSEG_MEM_HOST));
+    }
+    FeatureVolume x = x0 ? *x0 : guarded_set.unary;
     x.set_role(VolumeRole::solution);
-    const int w = cfg.resolved_temporal_window();
-    const std::size_t plane = static_cast<std::size_t>(shape.height) * shape.width;
-    RunTrace trace;
+    const std::uint32_t half = static_cast<std::uint32_t>(cfg.resolved_temporal_window());
+    const std::size_t frame = static_cast<std::size_t>(sh.height) * sh.width;
+    RunResult r;
     for (int iter = 1; iter <= cfg.iterations; ++iter) {
-        const auto tick = std::chrono::steady_clock::now();
-        FeatureVolume x_next(shape, VolumeRole::solution);
-        for (std::uint32_t i = 0; i < shape.frames; ++i) {
-            const std::uint32_t t0 = i >= static_cast<std::uint32_t>(w) ? i - w : 0;
-            const std::uint32_t t1 = std::min<std::uint32_t>(shape.frames - 1, i + w);
-            FeatureSet ws;
-            FeatureVolume x_w = slice_frames(x, t0, t1);
-            for (const auto& f : work.pairwise) ws.pairwise.push_back(slice_frames(f, t0, t1));
-            ws.unary = slice_frames(work.unary, t0, t1);
-            transform(ws.unary, ws.pairwise, x_w, i);
-            const FeatureVolume step = sfseg_step(x_w, ws, cfg);  // S^p of the slice on the GPU
-            std::memcpy(x_next.data() + i * plane, step.data() + (i - t0) * plane,
-                        sizeof(float) * plane);
+        const auto started = std::chrono::steady_clock::now();
+        FeatureVolume next(sh, VolumeRole::solution);
+        for (std::uint32_t t = 0; t < sh.frames; ++t) {
+            const std::uint32_t lo = t > half ? t - half : 0;
+            const std::uint32_t hi = std::min(sh.frames - 1, t + half);
+            FeatureSet win;
+            win.unary = window_of(guarded_set.unary, lo, hi);
+            for (const auto& f : guarded_set.pairwise) win.pairwise.push_back(window_of(f, lo, hi));
+            FeatureVolume xw = window_of(x, lo, hi);
+            transform(win.unary, win.pairwise, xw, t);
+            const FeatureVolume y = sfseg_step(xw, win, cfg);  // GPU, S^p of the window
+            const float* plane = y.data() + (t - lo) * frame;
+            std::copy(plane, plane + frame, next.data() + t * frame);
         }
-        auto [x_unit, norm] = normalize_l2(x_next);
-        x = project_binary(x_unit, iter, cfg);
+        auto [unit, norm] = normalize_l2(next);
+        x = project_binary(unit, iter, cfg);
         IterationRecord rec;
         rec.iter = iter;
         rec.l2_norm_pre_normalize = norm;
-        rec.wall_time_s =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - tick).count();
+        rec.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - started).count();
         if (reference) rec.angle_deg = angle_degrees(x, *reference);
         if (ground_truth) rec.iou = jaccard(threshold_final(x, cfg.threshold_frac), *ground_truth);
-        trace.iterations.push_back(rec);
+        r.trace.iterations.push_back(rec);
         if (observer) observer(iter, x);
     }
-    RunResult r;
     r.mask = threshold_final(x, cfg.final_threshold);
     r.soft = std::move(x);
-    r.trace = std::move(trace);
     return r;
 }
 
@@ -265,10 +341,32 @@ RunResult run(const FeatureSet& features, const SfsegConfig& cfg, const FeatureV
         return run_windowed(features, cfg, x0, reference, ground_truth, transform, observer);
     }
 
-    sfseg_ctx* c = ctx();
     const sfseg_params p = to_params(cfg);
     std::vector<const float*> F;
     for (const auto& f : features.pairwise) F.push_back(f.data());
+    if (num_gpus_of_env() > 1 && !observer && !reference && !ground_truth) {
+        // SFSEG_NUM_GPUS: time shards on the GPUs of this process
+        Multi* mu = multi();
+        std::lock_guard<std::mutex> lk(mu->mu);
+        RunResult r;
+        r.soft = FeatureVolume(shape, VolumeRole::solution);
+        r.mask.shape = shape;
+        r.mask.values.resize(shape.voxels());
+        std::vector<sfseg_iter_record> rec(static_cast<std::size_t>(cfg.iterations));
+        check(sfseg_multi_run(mu->m, shape.frames, shape.height, shape.width, static_cast<int32_t>(F.size()),
+                              features.unary.data(), F.data(), x0 ? x0->data() : nullptr, &p,
+                              r.soft.data(), r.mask.values.data(), rec.data(), SFSEG_MEM_HOST));
+        for (const auto& e : rec) {
+            IterationRecord ir;
+            ir.iter = e.iter;
+            ir.l2_norm_pre_normalize = e.l2_norm_pre_normalize;
+            ir.wall_time_s = e.wall_time_s;
+            r.trace.iterations.push_back(ir);
+        }
+        return r;
+    }
+    Lease lease;  // held for load, solve and download: the call is atomic
+    sfseg_ctx* c = lease.get();
     check(sfseg_load(c, shape.frames, shape.height, shape.width, static_cast<int32_t>(F.size()),
                      features.unary.data(), F.data(), x0 ? x0->data() : nullptr, SFSEG_MEM_HOST));
     RunResult r;
@@ -344,7 +442,8 @@ FeatureVolume convolve_separable(const FeatureVolume& v, const SeparableKernel3D
     s.validate();
     FeatureVolume out(s, v.role());
     const int32_t r[3] = {k.radii[0], k.radii[1], k.radii[2]};
-    check(sfseg_convolve_separable_taps(ctx(), s.frames, s.height, s.width, v.data(), r,
+    Lease lease;
+    check(sfseg_convolve_separable_taps(lease.get(), s.frames, s.height, s.width, v.data(), r,
                                         k.taps_t.data(), k.taps_y.data(), k.taps_x.data(),
                                         out.data(), SFSEG_MEM_HOST));
     return out;
@@ -355,7 +454,8 @@ FeatureVolume convolve_direct(const FeatureVolume& v, const SeparableKernel3D& k
     s.validate();
     FeatureVolume out(s, v.role());
     const int32_t r[3] = {k.radii[0], k.radii[1], k.radii[2]};
-    check(sfseg_convolve_direct_taps(ctx(), s.frames, s.height, s.width, v.data(), r,
+    Lease lease;
+    check(sfseg_convolve_direct_taps(lease.get(), s.frames, s.height, s.width, v.data(), r,
                                      k.taps_t.data(), k.taps_y.data(), k.taps_x.data(),
                                      out.data(), SFSEG_MEM_HOST));
     return out;

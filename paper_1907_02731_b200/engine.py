@@ -168,7 +168,10 @@ class Context:
         N.check(self._lib.sfseg_ctx_create(int(device), C.byref(h)))
         self.handle = h
         self.device = device
-        self.lock = threading.Lock()
+        # re-entrant: an IterationObserver may call the engine functions on
+        # the same context from inside run(); the library runs those on the
+        # context's scratch buffers, never on the resident problem
+        self.lock = threading.RLock()
 
     def close(self) -> None:
         if self.handle:
@@ -446,7 +449,7 @@ def run(features: FeatureSet, cfg: SfsegConfig, x0=None, reference=None, ground_
             gtb = _Buf(ground_truth, shape, dtype=np.uint8)
         except ShapeError:
             raise ShapeError("ground truth shape differs from features")
-    mem = _same_mem(bufs)
+    mem = _same_mem(bufs + [b for b in (refb, gtb) if b is not None])
     T, H, W = shape
     lib = ctx._lib
     soft = _empty_like(sb)

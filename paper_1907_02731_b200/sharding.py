@@ -200,14 +200,18 @@ class CudaBackend:
         self.ctx.close()
 
 
-def global_unit_range_guard(F_local: Sequence, group=None) -> None:
+def global_unit_range_guard(F_local: Sequence, group=None) -> list:
     """scale_channel_into_unit_range (engine.cpp:228-243) with the channel's
-    global min/max (all-reduce), applied in place to each rank's frames."""
+    global min/max (all-reduce). Returns the rank's channels: the caller's
+    own arrays where the guard leaves the bits alone, rescaled COPIES where
+    it applies (the reference rescales a copy too, engine.cpp:254-259; a
+    channel that aliases the unary volume must not change it)."""
     import torch
     import torch.distributed as dist
 
+    out = []
     for f in F_local:
-        t = f if isinstance(f, torch.Tensor) else torch.from_numpy(f)
+        t = f if isinstance(f, torch.Tensor) else torch.from_numpy(np.asarray(f))
         lo = t.min().reshape(1).clone()
         hi = t.max().reshape(1).clone()
         if dist.is_initialized():
@@ -215,12 +219,16 @@ def global_unit_range_guard(F_local: Sequence, group=None) -> None:
             dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
         lo_v, hi_v = float(lo.item()), float(hi.item())
         if lo_v >= 0.0 and hi_v <= 1.0:
-            continue  # leave the bits alone
+            out.append(f)  # leave the bits alone
+            continue
+        t = t.clone()
         if hi_v > lo_v:
             span = torch.tensor(hi_v, dtype=torch.float32) - torch.tensor(lo_v, dtype=torch.float32)
             t.sub_(torch.tensor(lo_v, dtype=torch.float32, device=t.device)).div_(span.to(t.device))
         else:
             t.fill_(min(max(lo_v, 0.0), 1.0))
+        out.append(t if isinstance(f, torch.Tensor) else t.numpy())
+    return out
 
 
 class ShardedSolver:
@@ -230,11 +238,14 @@ class ShardedSolver:
         self.b = backend
         self.rank, self.world, self.group = rank, world, group
 
-    def load(self, T, H, W, S_local, F_local, x0_local, halo, guard=True):
+    def load(self, T, H, W, S_local, F_local, x0_local, halo, allow_negative_affinity=False):
+        """allow_negative_affinity must match the SfsegConfig the solve runs
+        with (run() checks): off, the channels get the unit-range guard."""
         self.T, self.H, self.W, self.halo = T, H, W, halo
         self.t0, self.t1 = shard_range(T, self.world, self.rank)
-        if guard:
-            global_unit_range_guard(F_local, self.group)
+        self.allow_negative = bool(allow_negative_affinity)
+        if not self.allow_negative:
+            F_local = global_unit_range_guard(F_local, self.group)
         self.b.load(T, H, W, S_local, F_local, x0_local, self.t0, self.t1, halo)
         self.tmax = max(shard_range(T, self.world, r)[1] - shard_range(T, self.world, r)[0]
                         for r in range(self.world))
@@ -327,11 +338,19 @@ class ShardedSolver:
         return (torch.cat(sums).to(dev).contiguous(),
                 torch.cat(maxs).to(torch.float32).to(dev).contiguous())
 
+    def _check_cfg(self, cfg):
+        if bool(cfg.allow_negative_affinity) != self.allow_negative:
+            from .engine import ParameterError
+
+            raise ParameterError("allow_negative_affinity differs from the one the channels were "
+                                 "loaded with (the unit-range guard is applied at load)")
+
     def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
         """out: optional preallocated host (soft, mask) arrays for this rank's
         frames (the download lands there)."""
         import torch
 
+        self._check_cfg(cfg)
         params = cfg.to_params()
         self.b.cfg = cfg
         for it in range(1, cfg.iterations + 1):
@@ -350,8 +369,7 @@ class ShardedSolver:
 
     def solve_only(self, cfg) -> None:
         """The iteration loop without the download (benchmark timing)."""
-        import torch
-
+        self._check_cfg(cfg)
         params = cfg.to_params()
         self.b.cfg = cfg
         for it in range(1, cfg.iterations + 1):

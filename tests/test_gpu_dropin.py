@@ -52,3 +52,29 @@ def test_reference_acceptance_on_gpu_engine():
             assert err <= 1e-5
             continue
         assert ln.startswith("[PASS]"), ln
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_dropin_is_reentrant(arith):
+    """tests/cpp/dropin_threads.cpp: 4 host threads run sfseg::run at once
+    (results bit-equal to serial calls), and an observer calling sfseg_step /
+    normalize_l2 / threshold_final inside run() leaves the run unchanged."""
+    b = REF / "dropin_threads"
+    if not b.exists():
+        pytest.skip("dropin_threads not built (needs /root/reference at build time)")
+    env = dict(os.environ, SFSEG_ARITH=arith)
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+def test_reference_unit_tests_on_multi_gpu_engine():
+    """The same unchanged test_engine.cpp / test_conv3d.cpp with SFSEG_NUM_GPUS=2:
+    every plain run() goes through the in-process multi-GPU solve (two time
+    shards on the test GPU, SFSEG_MULTI_DEVICES=0,0)."""
+    b = REF / "unit_gpu"
+    if not b.exists():
+        pytest.skip("unit_gpu not built (needs /root/reference at build time)")
+    env = dict(os.environ, SFSEG_ARITH="exact", SFSEG_NUM_GPUS="2", SFSEG_MULTI_DEVICES="0,0")
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=600, env=env)
+    fails = [ln for ln in r.stdout.splitlines() if ln.startswith("[FAIL]")]
+    assert r.returncode == 0, "\n".join(fails) + r.stderr[-2000:]

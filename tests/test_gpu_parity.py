@@ -290,3 +290,29 @@ def test_step_generic_path_bit_exact(shape, alpha, p, radii, sigmas, C):
     got = E.sfseg_step(x, fs, cfg)
     want = Oracle().step(x, S, F, cfg)
     assert _equal_values(got, want)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_observer_may_call_the_engine_on_the_same_context(arith):
+    # the stateless operators run on the context's scratch buffers: calling
+    # them from an IterationObserver (same default context, same thread)
+    # neither deadlocks nor disturbs the resident solve
+    prob, fs, _ = _problem(2, frames=6)
+    fs = _crop(fs, 6, 60, 90)
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, "iterations": 5})
+    base = E.run(fs, cfg)
+    seen = []
+
+    def obs(it, x):
+        y = E.sfseg_step(x, fs, cfg)
+        u, n = E.normalize_l2(y)
+        E.threshold_final(u, 0.5)
+        seen.append(n)
+
+    res = E.run(fs, cfg, observer=obs)
+    assert len(seen) == cfg.iterations
+    assert np.array_equal(res.soft, base.soft)
+    assert np.array_equal(res.mask, base.mask)
+    # the observer's step of iterate k is the solve's step k+1: same norm
+    norms = [r.l2_norm_pre_normalize for r in res.trace.iterations]
+    assert np.allclose(seen[:-1], norms[1:], rtol=1e-5)

@@ -104,3 +104,53 @@ def test_shard_ranges_cover_and_balance():
             for a, b in rs:
                 lo, hi = buffer_range(T, a, b, 4)
                 assert lo == max(0, a - 4) and hi == min(T, b + 4)
+
+
+def _guard_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.shard_oracle_backend import OracleBackend
+
+        S, F = _problem(C=2)
+        F = [(2.0 * f - 0.5).astype(np.float32) for f in F]  # leaves [0, 1]: the guard rescales
+        T, H, W = S.shape
+        cfg = _cfg(False)
+        t0, t1 = shard_range(T, world, rank)
+        b0, b1 = buffer_range(T, t0, t1, cfg.kernel.radii[0])
+        mine = [np.ascontiguousarray(f[b0:b1]) for f in F]
+        before = [m.copy() for m in mine]
+        solver = ShardedSolver(OracleBackend(), rank, world)
+        solver.load(T, H, W, torch.from_numpy(S[b0:b1].copy()), mine, None, cfg.kernel.radii[0])
+        unchanged = all(np.array_equal(a, b) for a, b in zip(mine, before))
+        bad_cfg = False
+        try:
+            solver.run(SfsegConfig(**{**cfg.__dict__, "allow_negative_affinity": True,
+                                      "alpha": 1.0}))
+        except Exception:
+            bad_cfg = True
+        soft, mask, norms = solver.run(cfg)
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), soft=soft, unchanged=unchanged,
+                 bad_cfg=bad_cfg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_unit_range_guard_uses_global_range_on_copies(tmp_path):
+    """engine.cpp:254-259: channels outside [0, 1] are rescaled with the
+    channel's GLOBAL min/max (an all-reduce across ranks), on copies (the
+    caller's arrays keep their bits), and a solve whose config disagrees with
+    the guard decision taken at load is refused."""
+    from tests.oracle_lib import Oracle
+
+    world = 2
+    mp.spawn(_guard_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(tmp_path / f"g{r}.npz") for r in range(world)]
+    assert all(bool(p["unchanged"]) for p in parts)
+    assert all(bool(p["bad_cfg"]) for p in parts)
+    soft = np.concatenate([p["soft"] for p in parts])
+    S, F = _problem(C=2)
+    F = [(2.0 * f - 0.5).astype(np.float32) for f in F]
+    want, _, _, _ = Oracle().run(S, F, _cfg(False))
+    assert np.max(np.abs(soft.astype(np.float64) - want)) <= 1e-6
