@@ -419,13 +419,20 @@ def measure_config(gpu, idx, arith, steps, warmup, hbm, hbm_src, fp32_peak, cloc
     times."""
     from paper_1907_02731_b200 import synth
 
+    import torch
+
     probs = synth.config(idx)
     tot_vox_it, tot_ms, fused_ms, nv, launches = 0.0, 0.0, 0.0, 0, 0
+    pinned = []  # c3: the batch's inputs in pinned host memory, for the batch e2e below
     for prob in probs:
         fs, _ = prob.generate()
         cfg = prob.cfg
         cfg.arith = arith
         F = [fs.unary] if prob.spec.feature_mode == synth.FEAT_SAME else fs.pairwise
+        if idx == 3:
+            hs = torch.empty(prob.shape, dtype=torch.float32, pin_memory=True)
+            hs.numpy()[...] = fs.unary
+            pinned.append(hs)
         gpu.load(fs.unary, F)
         ms, fk, lpi = gpu.timed_solves(cfg, steps, warmup, clocks)
         n = prob.voxels()
@@ -448,7 +455,46 @@ def measure_config(gpu, idx, arith, steps, warmup, hbm, hbm_src, fp32_peak, cloc
            "shape": list(prob.shape) if idx != 3 else [list(p.shape) for p in probs],
            "channels": prob.channels, "radii": list(cfg.kernel.radii),
            "sigmas": list(cfg.kernel.sigmas), "iterations": cfg.iterations}
+    if idx == 3:
+        out["e2e"] = batch_e2e(gpu, pinned, cfg, nvox)
     return out
+
+
+def batch_e2e(gpu, pinned, cfg, nvox):
+    """The c3 batch end to end through sfseg_run_batch (include/sfseg_cuda.h):
+    pinned host inputs -> soft + mask in pinned host memory, for 1, 2 and 3
+    contexts on the device (with more than one, a clip's transfers run under
+    another clip's solve). Wall clock around the one C-ABI call."""
+    import torch
+
+    E = gpu.E
+    clips = [E.FeatureSet(h.numpy(), [h.numpy()]) for h in pinned]  # f = S: one upload per clip
+    outs = [(torch.empty(h.shape, dtype=torch.float32, pin_memory=True).numpy(),
+             torch.empty(h.shape, dtype=torch.uint8, pin_memory=True).numpy()) for h in pinned]
+    by = {}
+    extra = []
+    try:
+        for nctx in (1, 2, 3):
+            while len(extra) < nctx - 1:
+                extra.append(E.Context(gpu.ctx.device))
+            ctxs = [gpu.ctx] + extra[:nctx - 1]
+            E.run_batch(clips, cfg, ctxs=ctxs, outputs=outs)  # warms buffers and pools
+            ts = []
+            for _ in range(2):
+                t0 = time.perf_counter()
+                E.run_batch(clips, cfg, ctxs=ctxs, outputs=outs)
+                ts.append(time.perf_counter() - t0)
+            by[nctx] = nvox * cfg.iterations / (sum(ts) / len(ts))
+    finally:
+        for c in extra:
+            c.close()
+    best = max(by, key=by.get)
+    return {"value": by[best], "unit": UNIT, "contexts": best,
+            "by_contexts": {str(k): v for k, v in by.items()},
+            "h2d_bytes_per_step": nvox * 4, "d2h_bytes_per_step": nvox * 5,
+            "inputs": "S per clip, passed once as unary and feature (f = S)",
+            "call": "sfseg_run_batch (include/sfseg_cuda.h): LPT queue over the contexts, "
+                    "load + solve + download per clip"}
 
 
 def main():
@@ -524,36 +570,30 @@ def main():
         mine = assign_clips([p.voxels() for p in probs], world)[rank]
         gpu = Gpu(local)
         tot_ms, my_vox, fused_ms, launches = 0.0, 0, 0.0, 0
-        e2e_s, h2d, d2h = 0.0, 0, 0
+        pinned = []
         for i in mine:
             p = probs[i]
             fs, _ = p.generate()
             c = p.cfg
             c.arith = args.arith
             S = torch.from_numpy(fs.unary).pin_memory()
+            pinned.append(S)
             gpu.load(fs.unary, [fs.unary])
             ms, fk, lpi = gpu.timed_solves(c, args.steps, args.warmup, clocks)
             tot_ms += ms
             fused_ms += fk * c.iterations
             my_vox += p.voxels()
             launches += args.steps * launches_per_solve(c, 1, args.arith, lpi)
-            soft = torch.empty(p.shape, dtype=torch.float32, pin_memory=True)
-            mask = torch.empty(p.shape, dtype=torch.uint8, pin_memory=True)
-            gpu.run_once(S, [S], c, soft, mask)  # warm
-            t0 = time.perf_counter()
-            for _ in range(args.e2e_steps):
-                gpu.run_once(S, [S], c, soft, mask)
-            e2e_s += (time.perf_counter() - t0) / args.e2e_steps
-            h2d += p.voxels() * 4
-            d2h += p.voxels() * 5
+        # end to end: this rank's clips through sfseg_run_batch (pinned host in and out)
+        be = batch_e2e(gpu, pinned, cfg, my_vox)
         barrier()
         total_ms = max_over_ranks(tot_ms)
-        e2e_s = max_over_ranks(e2e_s)
+        e2e_s = max_over_ranks(my_vox * iters / be["value"])
         all_vox = sum(p.voxels() for p in probs)
         value = all_vox * iters * args.steps / (total_ms * 1e-3)
         fms_iter = fused_ms / iters  # this rank's clips (rank 0 prints)
-        e2e = {"value": all_vox * iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "inputs": "each clip's S, passed once as unary and feature"}
+        e2e = dict(be, value=all_vox * iters / e2e_s, h2d_bytes_per_step=all_vox * 4,
+                   d2h_bytes_per_step=all_vox * 5)
         rl = roofline(cfg, 1, my_vox, fms_iter, hbm, hbm_src, fp32_peak, _traffic(3, args.arith))
         rl["kernel"] = kernel_name(cfg, 1, args.arith)
         gpu_launches = launches

@@ -409,6 +409,36 @@ int sfseg_multi_run(sfseg_multi* m, uint32_t frames, uint32_t height, uint32_t w
                     const float* x0, const sfseg_params* p, float* soft, uint8_t* mask,
                     sfseg_iter_record* records, int32_t mem);
 
+/* ---- batches of independent clips (BASELINE configs[3]) --
+ * The reference solves one video per run() call (engine.cpp:247); a batch is
+ * a loop of calls. sfseg_run_batch runs that loop over a set of contexts:
+ * clips are taken largest first (longest-processing-time order, by voxel
+ * count) by whichever context is free next, one host thread per context.
+ * Contexts on different devices shard the batch across GPUs with no
+ * data-path collective; several contexts on ONE device pipeline it — the
+ * upload of one clip and the download of another run on the copy engines
+ * under the solve of a third. Every clip's result is what sfseg_run returns
+ * for it alone (bit-identical, whatever the assignment). */
+typedef struct sfseg_clip {
+    uint32_t frames, height, width;
+    int32_t channels;
+    const float* unary;
+    const float* const* pairwise; /* array of `channels` pointers */
+    const float* x0;              /* NULL: X0 = S */
+    float* soft;                  /* out, may be NULL */
+    uint8_t* mask;                /* out, may be NULL */
+    sfseg_iter_record* records;   /* out, may be NULL; p->iterations entries */
+    int32_t status;               /* out: SFSEG_OK or this clip's error code */
+    int32_t worker;               /* out: index into ctxs of the context that ran it */
+    double wall_ms;               /* out: host time of this clip's load + solve + download */
+} sfseg_clip;
+
+/* Returns SFSEG_OK when every clip succeeded, else the status of the first
+ * failing clip in batch order (its message in sfseg_last_error); the other
+ * clips still run. ctxs must be distinct contexts. */
+int sfseg_run_batch(sfseg_ctx* const* ctxs, int32_t nctx, sfseg_clip* clips, int32_t nclips,
+                    const sfseg_params* p, int32_t mem);
+
 #ifdef __cplusplus
 }
 #endif

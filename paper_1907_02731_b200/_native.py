@@ -141,6 +141,18 @@ class ShardIO(C.Structure):
     ]
 
 
+class Clip(C.Structure):
+    """sfseg_clip — one entry of sfseg_run_batch (include/sfseg_cuda.h)."""
+
+    _fields_ = [
+        ("frames", C.c_uint32), ("height", C.c_uint32), ("width", C.c_uint32),
+        ("channels", C.c_int32),
+        ("unary", C.c_void_p), ("pairwise", C.c_void_p), ("x0", C.c_void_p),
+        ("soft", C.c_void_p), ("mask", C.c_void_p), ("records", C.c_void_p),
+        ("status", C.c_int32), ("worker", C.c_int32), ("wall_ms", C.c_double),
+    ]
+
+
 _lib = None
 
 _P = C.c_void_p
@@ -184,6 +196,7 @@ _SIGS = {
                                   _P, _I32]),
     "sfseg_run": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, C.POINTER(Params), _P, _P,
                             C.POINTER(IterRecord), _I32]),
+    "sfseg_run_batch": (C.c_int, [_P, _I32, C.POINTER(Clip), _I32, C.POINTER(Params), _I32]),
     "sfseg_step": (C.c_int, [_P, _U32, _U32, _U32, _I32, _P, _P, _P, C.POINTER(Params), _P, _I32]),
     "sfseg_step_channel": (C.c_int, [_P, _U32, _U32, _U32, _P, _P, _P, C.POINTER(Params), _P, _I32]),
     "sfseg_normalize_l2": (C.c_int, [_P, _U32, _U32, _U32, _P, _P, C.POINTER(C.c_double), _I32]),

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sfseg_cuda.h"
@@ -490,6 +492,11 @@ struct sfseg_ctx {
     void* pin_small = nullptr;  // pinned arena of small host transfers (pin_slot)
     size_t pin_small_cap = 0, pin_small_used = 0;
 
+    // volume buffers are allocated with cap_elems >= vol_elems() floats: a
+    // context that loads problems of several shapes (sfseg_run_batch, a clip
+    // after a clip) reallocates only when a problem outgrows them
+    size_t cap_elems = 0;
+    int frames_cap = 0;
     size_t vol_elems() const { return static_cast<size_t>(T) * H * P; }
     Vol vol(float* p) const { return Vol{p, T, H, W, P}; }
     int Tout() const { return out_t1 - out_t0; }
@@ -503,16 +510,61 @@ struct sfseg_ctx {
 
 namespace {
 
+// SFSEG_DEBUG_GUARD=1 (tests/test_gpu_guardbands.py; the pool's GPUs refuse
+// compute-sanitizer): every volume buffer gets a guard band of kGuard floats
+// on either side, bands AND interior are filled with a NaN pattern instead of
+// zeros, and sfseg_debug_check_guards counts band words that changed. An
+// out-of-bounds store lands in a band; a read of memory no kernel wrote (or
+// of the pitch padding) puts a NaN in the result.
+constexpr size_t kGuard = 16384;            // floats per band (64 KiB, keeps 128-B alignment)
+constexpr uint32_t kPoison = 0x7fc0dead;    // a quiet NaN
+bool guard_mode() {
+    static const bool on = env_flag("SFSEG_DEBUG_GUARD");
+    return on;
+}
+std::mutex g_guard_mu;
+std::vector<std::pair<float*, size_t>> g_guarded;  // (user pointer, floats) of live guarded buffers
+
+__global__ void k_fill_u32(uint32_t* p, size_t n, uint32_t v) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+void poison_fill(float* p, size_t n, cudaStream_t s) {
+    k_fill_u32<<<1184, 256, 0, s>>>(reinterpret_cast<uint32_t*>(p), n, kPoison);
+    launched(s, "k_fill_u32");
+}
+
 void dfree(float*& p) {
-    if (p) cudaFree(p);
+    if (p) {
+        if (guard_mode()) {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            for (size_t i = 0; i < g_guarded.size(); ++i)
+                if (g_guarded[i].first == p) {
+                    g_guarded.erase(g_guarded.begin() + i);
+                    break;
+                }
+            cudaFree(p - kGuard);
+        } else {
+            cudaFree(p);
+        }
+    }
     p = nullptr;
 }
 
 float* dalloc_vol(sfseg_ctx* c) {
     float* p = nullptr;
-    ck(cudaMalloc(&p, c->vol_elems() * sizeof(float)), "cudaMalloc volume");
+    const size_t n = std::max(c->cap_elems, c->vol_elems());
+    if (guard_mode()) {
+        ck(cudaMalloc(&p, (n + 2 * kGuard) * sizeof(float)), "cudaMalloc volume");
+        poison_fill(p, n + 2 * kGuard, c->stream);
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        g_guarded.emplace_back(p + kGuard, n);
+        return p + kGuard;
+    }
+    ck(cudaMalloc(&p, n * sizeof(float)), "cudaMalloc volume");
     // zero the pitch padding once; kernels never read past W, TMA treats it as OOB
-    ck(cudaMemsetAsync(p, 0, c->vol_elems() * sizeof(float), c->stream), "memset");
+    ck(cudaMemsetAsync(p, 0, n * sizeof(float), c->stream), "memset");
     return p;
 }
 
@@ -556,6 +608,9 @@ void release_problem(sfseg_ctx* c) {
     c->part = nullptr;
     c->frame_sum = nullptr;
     c->frame_max = nullptr;
+    c->part_elems = 0;
+    c->frames_cap = 0;
+    c->cap_elems = 0;
     c->loaded = false;
     c->resident = false;
     c->cur = -1;
@@ -588,7 +643,29 @@ void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int 
     if (c->loaded && c->T == (int)T && c->H == (int)H && c->W == (int)W && c->C == C &&
         c->Tg == Tg && c->buf_t0 == buf_t0 && c->out_t0 == out_t0 && c->out_t1 == out_t1)
         return;
-    release_problem(c);
+    // the buffers of an earlier problem are kept when this one fits in them
+    // (same channel count, no more floats per volume): no cudaFree/cudaMalloc
+    // (both synchronise the device) between the clips of a batch
+    const int P = round_up(static_cast<int>(W), 32);
+    const size_t need = static_cast<size_t>(T) * H * P;
+    const bool reuse = c->loaded && c->C == C && need <= c->cap_elems;
+    const bool same_rows = reuse && c->W == (int)W && c->P == P;
+    if (reuse) {
+        if (c->guard_applied)
+            for (size_t i = 0; i < c->Fw.size(); ++i)
+                if (c->Fw[i] != c->F[i]) dfree(c->Fw[i]);
+        c->Fw = c->F;
+        c->guard_applied = false;
+        c->q_for.clear();
+        drop_peers(c);
+        c->resident = false;
+        c->cur = -1;
+        c->cur_u = false;
+        c->sp_p = NAN;
+    } else {
+        release_problem(c);
+        c->cap_elems = need;
+    }
     c->Tg = Tg;
     c->buf_t0 = buf_t0;
     c->out_t0 = out_t0;
@@ -597,22 +674,58 @@ void set_shape(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, int 
     c->T = T;
     c->H = H;
     c->W = W;
-    c->P = round_up(static_cast<int>(W), 32);
+    c->P = P;
     c->C = C;
     ++c->alloc_gen;
     c->in_valid = false;
-    c->S = dalloc_vol(c);
-    c->sp = dalloc_vol(c);
-    for (int i = 0; i < C; ++i) c->F.push_back(dalloc_vol(c));
-    c->Fw = c->F;
-    c->y[0] = dalloc_vol(c);
-    c->y[1] = dalloc_vol(c);
+    if (!reuse) {
+        c->S = dalloc_vol(c);
+        c->sp = dalloc_vol(c);
+        for (int i = 0; i < C; ++i) c->F.push_back(dalloc_vol(c));
+        c->Fw = c->F;
+        c->y[0] = dalloc_vol(c);
+        c->y[1] = dalloc_vol(c);
+    } else if (!same_rows) {
+        // a different row layout: the pitch padding (columns W .. P-1 of every
+        // row) must read as zero again
+        auto zero = [&](float* p) {
+            if (!p) return;
+            if (guard_mode()) {  // keep the padding poisoned (see dalloc_vol)
+                poison_fill(p, need, c->stream);
+                return;
+            }
+            ck(cudaMemsetAsync(p, 0, need * sizeof(float), c->stream), "memset");
+        };
+        zero(c->S);
+        zero(c->sp);
+        for (float* f : c->F) zero(f);
+        zero(c->y[0]);
+        zero(c->y[1]);
+        zero(c->x0);
+        zero(c->q);
+        for (float* t : c->tmp) zero(t);
+    }
     const int tout = c->Tout();
-    c->part_elems = static_cast<size_t>(tout) * c->nbands() * c->nhalves();
-    ck(cudaMalloc(&c->part, c->part_elems * sizeof(double)), "cudaMalloc partials");
-    ck(cudaMalloc(&c->frame_sum, std::max(tout, Tg) * sizeof(double)), "cudaMalloc frame sums");
-    ck(cudaMalloc(&c->frame_max, std::max(tout, Tg) * sizeof(float)), "cudaMalloc frame max");
-    ck(cudaMemsetAsync(c->frame_max, 0, std::max(tout, Tg) * sizeof(float), c->stream), "memset");
+    const size_t parts = static_cast<size_t>(tout) * c->nbands() * c->nhalves();
+    if (parts > c->part_elems) {
+        if (c->part) cudaFree(c->part);
+        c->part = nullptr;
+        c->part_elems = 0;
+        ck(cudaMalloc(&c->part, parts * sizeof(double)), "cudaMalloc partials");
+        c->part_elems = parts;
+    }
+    const int frames = std::max(tout, Tg);
+    if (frames > c->frames_cap) {
+        if (c->frame_sum) cudaFree(c->frame_sum);
+        if (c->frame_max) cudaFree(c->frame_max);
+        c->frame_sum = nullptr;
+        c->frame_max = nullptr;
+        c->frames_cap = 0;
+        ck(cudaMalloc(&c->frame_sum, frames * sizeof(double)), "cudaMalloc frame sums");
+        ck(cudaMalloc(&c->frame_max, frames * sizeof(float)), "cudaMalloc frame max");
+        c->frames_cap = frames;
+    }
+    ck(cudaMemsetAsync(c->frame_max, 0, frames * sizeof(float), c->stream), "memset");
     c->loaded = true;
 }
 
@@ -2125,6 +2238,60 @@ int sfseg_run(sfseg_ctx* c, uint32_t T, uint32_t H, uint32_t W, int32_t C, const
     });
 }
 
+int sfseg_run_batch(sfseg_ctx* const* ctxs, int32_t nctx, sfseg_clip* clips, int32_t nclips,
+                    const sfseg_params* p, int32_t mem) {
+    // The reference's batch is a loop of run() calls (one video each,
+    // engine.cpp:247). Here: a shared queue in LPT order, one host thread per
+    // context. On one device the contexts' copy-stream DMAs overlap the other
+    // contexts' kernels; on several devices the clips shard with no exchange.
+    std::vector<std::string> msgs;
+    const int rc = guarded([&] {
+        if (!ctxs || nctx < 1 || nclips < 0 || (nclips > 0 && !clips) || !p)
+            fail(SFSEG_ERR_PARAMETER, "null argument");
+        for (int i = 0; i < nctx; ++i) {
+            if (!ctxs[i]) fail(SFSEG_ERR_PARAMETER, "null ctx");
+            for (int j = 0; j < i; ++j)
+                if (ctxs[j] == ctxs[i]) fail(SFSEG_ERR_PARAMETER, "contexts must be distinct");
+        }
+        validate_params(p);
+        std::vector<int> order(nclips);
+        for (int i = 0; i < nclips; ++i) order[i] = i;
+        auto voxels = [&](int i) {
+            return static_cast<unsigned __int128>(clips[i].frames) * clips[i].height * clips[i].width *
+                   static_cast<unsigned>(std::max(1, clips[i].channels));
+        };
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return voxels(a) > voxels(b); });
+        msgs.assign(nclips, std::string());
+        std::atomic<int> next{0};
+        auto work = [&](int w) {
+            for (;;) {
+                const int k = next.fetch_add(1);
+                if (k >= nclips) return;
+                sfseg_clip& cl = clips[order[k]];
+                const auto t0 = std::chrono::steady_clock::now();
+                cl.worker = w;
+                cl.status = sfseg_run(ctxs[w], cl.frames, cl.height, cl.width, cl.channels, cl.unary,
+                                      cl.pairwise, cl.x0, p, cl.soft, cl.mask, cl.records, mem);
+                if (cl.status != SFSEG_OK) msgs[order[k]] = g_err;  // this thread's message
+                cl.wall_ms = std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count();
+            }
+        };
+        std::vector<std::thread> th;
+        const int nw = std::min<int>(nctx, std::max(1, nclips));
+        for (int w = 1; w < nw; ++w) th.emplace_back(work, w);
+        work(0);
+        for (auto& t : th) t.join();
+    });
+    if (rc != SFSEG_OK) return rc;
+    for (int i = 0; i < nclips; ++i)
+        if (clips[i].status != SFSEG_OK) {
+            g_err = "clip " + std::to_string(i) + ": " + msgs[i];
+            return clips[i].status;
+        }
+    return SFSEG_OK;
+}
+
 int sfseg_step(sfseg_ctx* owner, uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* x,
                const float* S, const float* const* F, const sfseg_params* p, float* out,
                int32_t mem) {
@@ -2936,6 +3103,60 @@ int sfseg_multi_run(sfseg_multi* m, uint32_t T, uint32_t H, uint32_t W, int32_t 
 }
 
 }  // extern "C"
+
+namespace {
+__global__ void k_guard_count(const uint32_t* lo, const uint32_t* hi, size_t n, uint32_t pat,
+                              unsigned long long* bad) {
+    unsigned long long mine = 0;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        mine += (lo[i] != pat) + (hi[i] != pat);
+    if (mine) atomicAdd(bad, mine);
+}
+}  // namespace
+
+// SFSEG_DEBUG_GUARD=1: counts the guard-band words of every live volume buffer
+// (all contexts of the process) that no longer hold the fill pattern, i.e.
+// out-of-bounds stores by any kernel since the buffer was allocated.
+// *buffers receives the number of buffers checked. Returns SFSEG_ERR_STATE
+// when the library is not in guard mode.
+extern "C" int sfseg_debug_check_guards(unsigned long long* bad_words, int32_t* buffers) {
+    return guarded([&] {
+        if (!bad_words) fail(SFSEG_ERR_PARAMETER, "null argument");
+        if (!guard_mode()) fail(SFSEG_ERR_STATE, "SFSEG_DEBUG_GUARD is not set");
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        unsigned long long total = 0;
+        for (auto& [ptr, n] : g_guarded) {
+            cudaPointerAttributes at{};
+            ck(cudaPointerGetAttributes(&at, ptr), "pointer attributes");
+            ck(cudaSetDevice(at.device), "cudaSetDevice");
+            ck(cudaDeviceSynchronize(), "sync");
+            unsigned long long* d = nullptr;
+            ck(cudaMalloc(&d, sizeof *d), "malloc");
+            ck(cudaMemset(d, 0, sizeof *d), "memset");
+            k_guard_count<<<64, 256>>>(reinterpret_cast<const uint32_t*>(ptr - kGuard),
+                                       reinterpret_cast<const uint32_t*>(ptr + n), kGuard, kPoison, d);
+            unsigned long long h = 0;
+            ck(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost), "D2H");
+            cudaFree(d);
+            total += h;
+        }
+        *bad_words = total;
+        if (buffers) *buffers = static_cast<int32_t>(g_guarded.size());
+    });
+}
+
+// test hook of the checker itself: overwrites `words` words of the first live
+// buffer's upper guard band (what a kernel storing past its buffer would do)
+extern "C" int sfseg_debug_poke_guard(int32_t words) {
+    return guarded([&] {
+        if (!guard_mode()) fail(SFSEG_ERR_STATE, "SFSEG_DEBUG_GUARD is not set");
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        if (g_guarded.empty() || words < 0 || static_cast<size_t>(words) > kGuard)
+            fail(SFSEG_ERR_PARAMETER, "nothing to poke");
+        ck(cudaMemset(g_guarded[0].first + g_guarded[0].second, 0, words * sizeof(float)), "poke");
+    });
+}
 
 #ifdef SFK_TRACE
 extern "C" int sfseg_debug_trace(unsigned long long* out) {

@@ -41,6 +41,7 @@ __all__ = [
     "KernelConfig", "SfsegConfig", "FeatureSet", "IterationRecord", "RunTrace", "RunResult",
     "SeparableKernel3D", "make_gaussian_kernel", "convolve_separable", "sfseg_step",
     "sfseg_step_channel", "normalize_l2", "project_binary", "threshold_final", "run",
+    "run_once", "run_batch",
     "separable_convolution_count", "Context", "default_context", "Error", "ParameterError",
     "ShapeError", "ValidationError", "DegenerateSolutionError", "CapacityError", "IoError",
     "FormatError", "CorruptionError", "run_files", "volume_shape", "affinity_matvec",
@@ -144,6 +145,8 @@ class RunResult:
     soft: np.ndarray
     mask: np.ndarray
     trace: RunTrace
+    worker: int = 0       # run_batch: index of the context that ran the clip
+    wall_ms: float = 0.0  # run_batch: host time of the clip's load + solve + download
 
 
 @dataclass
@@ -490,6 +493,77 @@ def run(features: FeatureSet, cfg: SfsegConfig, x0=None, reference=None, ground_
         ob, mb = _Buf(soft, writable=True), _Buf(mask, writable=True, dtype=np.uint8)
         N.check(lib.sfseg_download(ctx.handle, float(cfg.final_threshold), ob.ptr, mb.ptr, mem))
     return RunResult(soft, mask, trace)
+
+
+def run_batch(clips: Sequence[FeatureSet], cfg: SfsegConfig, x0s: Optional[Sequence] = None,
+              ctxs: Optional[Sequence[Context]] = None, outputs: Optional[Sequence] = None):
+    """A batch of independent videos (BASELINE configs[3]): the reference runs
+    one video per run() call (engine.cpp:247), so a batch is a loop of calls;
+    sfseg_run_batch runs that loop over ``ctxs`` — largest clip first, each
+    context on its own host thread. Contexts on one device overlap one clip's
+    transfers with another's solve; contexts on several devices shard the
+    batch (no collective). Every result equals run_once() of that clip alone.
+
+    ``outputs``: optional list of (soft, mask) host arrays to fill (e.g. pinned
+    buffers); otherwise numpy arrays are allocated. Returns a list of
+    RunResult in batch order; the first failing clip raises its error."""
+    if ctxs is None:
+        ctxs = [default_context()]
+    lib = ctxs[0]._lib
+    p = cfg.to_params()
+    N.check(lib.sfseg_params_validate(C.byref(p)))
+    n = len(clips)
+    arr = (N.Clip * max(n, 1))()
+    keep = []
+    results = []
+    mem = None
+    for i, fs in enumerate(clips):
+        sb = _Buf(fs.unary)
+        shape = _shape3(sb.shape)
+        if len(fs.pairwise) == 0:
+            raise ValidationError("feature set needs at least one pairwise channel")
+        fbs = [sb if f is fs.unary else _Buf(f, shape) for f in fs.pairwise]
+        x0b = _Buf(x0s[i], shape) if x0s is not None and x0s[i] is not None else None
+        m = _same_mem([sb] + fbs + ([x0b] if x0b else []))
+        if mem is not None and m != mem:
+            raise ValidationError("mixing host and device volumes in one call")
+        mem = m
+        if outputs is not None:
+            soft, mask = outputs[i]
+        else:
+            soft, mask = _empty_like(sb), _empty_like(sb, np.uint8)
+        ob, mb = _Buf(soft, shape, writable=True), _Buf(mask, shape, writable=True, dtype=np.uint8)
+        recs = (N.IterRecord * cfg.iterations)()
+        fp = _channel_ptrs(fbs)
+        keep.append((sb, fbs, x0b, ob, mb, recs, fp))
+        T, H, W = shape
+        c = arr[i]
+        c.frames, c.height, c.width, c.channels = T, H, W, len(fbs)
+        c.unary = sb.ptr
+        c.pairwise = C.cast(fp, C.c_void_p)
+        c.x0 = x0b.ptr if x0b else None
+        c.soft, c.mask = ob.ptr, mb.ptr
+        c.records = C.cast(recs, C.c_void_p)
+        results.append((soft, mask, recs))
+    handles = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+    locks = [c.lock for c in ctxs]
+    for lk in locks:
+        lk.acquire()
+    try:
+        N.check(lib.sfseg_run_batch(C.cast(handles, C.c_void_p), len(ctxs), arr, n, C.byref(p),
+                                    mem if mem is not None else N.SFSEG_MEM_HOST))
+    finally:
+        for lk in locks:
+            lk.release()
+    out = []
+    for i, (soft, mask, recs) in enumerate(results):
+        trace = RunTrace([IterationRecord(r.iter, r.l2_norm_pre_normalize, wall_time_s=r.wall_time_s)
+                          for r in recs])
+        res = RunResult(soft, mask, trace)
+        res.worker = int(arr[i].worker)
+        res.wall_ms = float(arr[i].wall_ms)
+        out.append(res)
+    return out
 
 
 def run_once(features: FeatureSet, cfg: SfsegConfig, x0=None,

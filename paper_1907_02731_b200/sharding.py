@@ -61,20 +61,34 @@ def assign_clips(voxels: Sequence[int], world: int) -> List[List[int]]:
     return out
 
 
-def run_clips(problems, rank: int, world: int, ctx=None, arith: Optional[str] = None):
-    """Runs this rank's share of a batch of independent problems (clip
-    sharding, no collective). Returns {clip index: RunResult}."""
+def run_clips(clips, cfg, rank: int = 0, world: int = 1, ctxs=None, x0s=None):
+    """Clip sharding: this rank's LPT share of a caller's
+    batch of independent videos, run through sfseg_run_batch on ``ctxs`` (one
+    or more contexts of this rank's GPU; two pipeline transfers under
+    solves). No data-path collective. ``clips``: FeatureSets (all of the
+    batch, so every rank computes the same assignment from the voxel counts).
+    Returns {clip index: RunResult}."""
+    from . import engine as E
+
+    vox = [int(np.prod(np.shape(c.unary))) for c in clips]
+    mine = assign_clips(vox, world)[rank]
+    res = E.run_batch([clips[i] for i in mine], cfg,
+                      x0s=None if x0s is None else [x0s[i] for i in mine], ctxs=ctxs)
+    return dict(zip(mine, res))
+
+
+def run_problems(problems, rank: int, world: int, ctxs=None, arith: Optional[str] = None):
+    """run_clips for synthetic problems (synth.config(3)): only this rank's
+    clips are generated. All clips of a config share one SfsegConfig."""
     from . import engine as E
 
     mine = assign_clips([p.voxels() for p in problems], world)[rank]
-    ctx = ctx or E.default_context()
-    out = {}
-    for i in mine:
-        prob = problems[i]
-        fs, _ = prob.generate()
-        cfg = prob.cfg if arith is None else E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith})
-        out[i] = E.run(fs, cfg, ctx=ctx)
-    return out
+    if not mine:
+        return {}
+    cfg0 = problems[mine[0]].cfg
+    cfg = cfg0 if arith is None else E.SfsegConfig(**{**cfg0.__dict__, "arith": arith})
+    clips = [problems[i].generate()[0] for i in mine]
+    return dict(zip(mine, E.run_batch(clips, cfg, ctxs=ctxs)))
 
 
 def buffer_range(T: int, t0: int, t1: int, halo: int) -> Tuple[int, int]:

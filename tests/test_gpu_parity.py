@@ -260,10 +260,10 @@ def test_run_multichannel_configs_cropped_match_reference(idx, crop, arith):
 def test_run_c3_clips_match_reference():
     # c3: independent clips (each its own problem, own norm); every clip of
     # the batch T-cropped to 12 frames, full resolution
-    from paper_1907_02731_b200.sharding import run_clips
+    from paper_1907_02731_b200.sharding import run_problems
 
     clips = synth.config(3, frames=12)[:4]
-    results = run_clips(clips, rank=0, world=1)  # the clip-sharded driver, one rank
+    results = run_problems(clips, rank=0, world=1)  # the clip-sharded driver, one rank
     assert sorted(results) == list(range(len(clips)))
     for i, prob in enumerate(clips):
         fs, _ = prob.generate()
