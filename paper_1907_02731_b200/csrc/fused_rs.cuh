@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
         auto plane = [&](auto slot_c) {
             constexpr int S_ = decltype(slot_c)::value;
             constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
-            const int slot = TMR ? rslot : S_;
+            [[maybe_unused]] const int slot = TMR ? rslot : S_;
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const bool emit = q.p - RT >= q.ta;

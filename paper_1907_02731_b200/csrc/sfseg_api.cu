@@ -203,7 +203,7 @@ struct FusedVariant {
 #ifndef SFK_NWA
 #define SFK_NWA 8
 #endif
-template <int RT, int R, bool FMA, int NWA = SFK_NWA>
+template <int RT, int R, int NWA = SFK_NWA>
 FusedVariant variant_ws() {
 #ifndef SFK_STAGES
 #define SFK_STAGES 2
@@ -214,11 +214,11 @@ FusedVariant variant_ws() {
     v.r = R;
     v.ty = G::TY;
     v.tx = G::TX;
-    v.fma = FMA;
+    v.fma = false;  // EXACT only (fused_ws.cuh)
     v.smem = G::SMEM_BYTES;
     v.threads = G::NT;
-    v.kernel = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, FMA, NWA, false>;
-    v.kernel_acc = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, FMA, NWA, true>;
+    v.kernel = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, NWA, false>;
+    v.kernel_acc = sfk::fused_step_ws<RT, R, 1, SFK_STAGES, NWA, true>;
     v.box_w = G::BW;
     v.box_h = G::BH;
     return v;
@@ -294,14 +294,12 @@ const std::vector<McVariant>& mc_variants() {
     return v;
 }
 
-#define SFK_VARIANTS_WS(FMA_)                                                             \
-    variant_ws<1, 2, FMA_>(), variant_ws<1, 3, FMA_>(), variant_ws<2, 4, FMA_>(),         \
-        variant_ws<2, 5, FMA_>()
+#define SFK_VARIANTS_WS() variant_ws<1, 2>(), variant_ws<1, 3>(), variant_ws<2, 4>(), variant_ws<2, 5>()
 
 // EXACT runs the warp-specialised kernel (fused_ws.cuh), FAST the
 // register-streamed one (fused_rs.cuh).
 const std::vector<FusedVariant>& variants() {
-    static const std::vector<FusedVariant> v = {SFK_VARIANTS_WS(false), SFK_VARIANTS_RS()};
+    static const std::vector<FusedVariant> v = {SFK_VARIANTS_WS(), SFK_VARIANTS_RS()};
     return v;
 }
 
@@ -3158,8 +3156,3 @@ extern "C" int sfseg_debug_poke_guard(int32_t words) {
     });
 }
 
-#ifdef SFK_TRACE
-extern "C" int sfseg_debug_trace(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, sfk_trace, sizeof(sfk_trace)) == cudaSuccess ? 0 : 1;
-}
-#endif
