@@ -166,8 +166,8 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-CUtensorMap make_tmap(const float* base, int frames, int H, int W, int pitch, int box_w,
-                      int box_h) {
+CUtensorMap encode_tmap(const float* base, int frames, int H, int W, int pitch, int box_w,
+                        int box_h) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                                 static_cast<cuuint64_t>(frames)};
@@ -182,6 +182,40 @@ CUtensorMap make_tmap(const float* base, int frames, int H, int W, int pitch, in
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SFSEG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return m;
+}
+
+// A solve encodes the same few descriptors every iteration (the two iterate
+// buffers alternate; S^p and the channels never change): a small per-thread
+// cache keyed by every encoded field. A descriptor holds only the address
+// and the geometry, so an entry stays valid when the buffer is reallocated
+// at the same address. Small solves are host-bound without it (c0: ~15 us of
+// kernels per iteration against five driver calls).
+CUtensorMap make_tmap(const float* base, int frames, int H, int W, int pitch, int box_w,
+                      int box_h) {
+    struct Key {
+        const float* base;
+        int frames, H, W, pitch, box_w, box_h;
+        bool operator==(const Key& o) const {
+            return base == o.base && frames == o.frames && H == o.H && W == o.W && pitch == o.pitch &&
+                   box_w == o.box_w && box_h == o.box_h;
+        }
+    };
+    struct Entry {
+        Key k;
+        CUtensorMap m;
+    };
+    constexpr int kSlots = 64;  // direct-mapped
+    thread_local std::vector<Entry> cache(kSlots, Entry{Key{nullptr, 0, 0, 0, 0, 0, 0}, CUtensorMap{}});
+    const Key k{base, frames, H, W, pitch, box_w, box_h};
+    size_t h = reinterpret_cast<uintptr_t>(base) >> 8;
+    h = h * 0x9e3779b97f4a7c15ull + static_cast<size_t>(box_w) * 131 + static_cast<size_t>(box_h) * 31 +
+        static_cast<size_t>(frames);
+    Entry& e = cache[(h >> 20) % kSlots];
+    if (!(e.k == k)) {
+        e.m = encode_tmap(base, frames, H, W, pitch, box_w, box_h);
+        e.k = k;
+    }
+    return e.m;
 }
 
 // ---- fused kernel registry -------------------------------------------------

@@ -161,3 +161,26 @@ def test_context_reuse_across_shapes_is_clean():
             fresh.close()
     finally:
         ctx.close()
+
+
+def test_full_c3_batch_equals_one_call_per_clip():
+    # BASELINE configs[3] at full size: 14 clips, T in [21, 279], two
+    # resolutions, 25 iterations, through three contexts of the GPU
+    probs = synth.config(3)
+    cfg = E.SfsegConfig(**{**probs[0].cfg.__dict__, "arith": "fast"})
+    clips = []
+    for p in probs:
+        fs, _ = p.generate()
+        clips.append(E.FeatureSet(fs.unary, [fs.unary]))  # f = S, passed once
+    ctxs = [E.Context(0) for _ in range(3)]
+    try:
+        got = E.run_batch(clips, cfg, ctxs=ctxs)
+        assert len({r.worker for r in got}) > 1  # the queue really spread the clips
+        for fs, r in zip(clips, got):
+            one = E.run_once(fs, cfg, ctx=ctxs[0])
+            assert np.array_equal(r.soft, one.soft)
+            assert np.array_equal(r.mask, one.mask)
+            assert np.isfinite(r.soft).all() and abs(float(np.linalg.norm(r.soft.astype(np.float64))) - 1.0) < 1e-5
+    finally:
+        for c in ctxs:
+            c.close()
