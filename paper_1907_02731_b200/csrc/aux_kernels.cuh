@@ -225,6 +225,7 @@ __global__ void k_partials(Vol v, double* part, float* frame_max, int nbands, in
 __global__ void k_finalize_frames(const double* part, int per_frame, double* frame_sum,
                                   int t0) {
     __shared__ double s[kAuxThreads];
+    griddep_wait();  // PDL: the step's partials are complete
     const int t = blockIdx.x + t0;
     const double* p = part + static_cast<size_t>(t) * per_frame;
     double acc = 0.0;
@@ -292,6 +293,7 @@ __device__ __forceinline__ void finalize_total_block(const double* frame_sum, fl
 __global__ void k_finalize_total(const double* frame_sum, float* frame_max, int T,
                                  IterState* st, double* norms, int iter_index, int mode_next,
                                  double lambda, double threshold_frac) {
+    griddep_wait();  // PDL: the frame sums (or their gather) are complete
     finalize_total_block(frame_sum, frame_max, T, st, norms, iter_index, mode_next, lambda,
                          threshold_frac);
 }

@@ -1228,8 +1228,8 @@ bool launch_step(sfseg_ctx* c, const HostKernel& k, double alpha, const float* x
 
 void frame_sums(sfseg_ctx* c) {
     const int per_frame = c->nbands() * c->nhalves();
-    sfk::k_finalize_frames<<<c->Tout(), sfk::kAuxThreads, 0, c->stream>>>(c->part, per_frame,
-                                                                        c->frame_sum, 0);
+    launch_pdl(sfk::k_finalize_frames, c->Tout(), sfk::kAuxThreads, 0, c->stream,
+               static_cast<const double*>(c->part), per_frame, c->frame_sum, 0);
     launched(c->stream, "k_finalize_frames");
 }
 
@@ -1241,8 +1241,13 @@ void finalize(sfseg_ctx* c, IterState* st, double* norms, int iter_index, int mo
     launched(c->stream, "k_finalize");
 }
 
+// the state goes by value in the launch parameters (no host buffer that has
+// to outlive the call: the sharded loop may be captured into a CUDA graph)
+__global__ void k_set_state(IterState* dst, const IterState s) { *dst = s; }
+
 void set_state(sfseg_ctx* c, IterState* dst, const IterState& s) {
-    ck(cudaMemcpyAsync(dst, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state");
+    k_set_state<<<1, 1, 0, c->stream>>>(dst, s);
+    launched(c->stream, "k_set_state");
 }
 
 IterState get_state(sfseg_ctx* c, const IterState* src) {
@@ -2627,7 +2632,10 @@ int sfseg_shard_step(sfseg_ctx* c, const sfseg_params* p, int32_t iter, sfseg_sh
             c->cur = -1;
             c->cur_u = false;
         }
-        ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
+        // k_finalize_total leaves frame_max zeroed for the next iteration
+        if (iter == 1)
+            ck(cudaMemsetAsync(c->frame_max, 0, std::max(c->Tout(), c->Tg) * sizeof(float), c->stream),
+               "memset");
         const float* src = c->cur < 0 ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
         const int dst = c->cur < 0 ? 0 : 1 - c->cur;
         c->peer_push_dst = dst;
@@ -2757,8 +2765,11 @@ int sfseg_shard_finalize(sfseg_ctx* c, const sfseg_params* p, int32_t iter,
         validate_params(p);
         const cudaMemcpyKind kind =
             mem == SFSEG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        ck(cudaMemcpyAsync(c->frame_sum, frame_sum, c->Tg * sizeof(double), kind, c->stream), "sums");
-        ck(cudaMemcpyAsync(c->frame_max, frame_max, c->Tg * sizeof(float), kind, c->stream), "max");
+        // one rank: the gathered arrays are this shard's own (nothing to copy)
+        if (frame_sum != c->frame_sum)
+            ck(cudaMemcpyAsync(c->frame_sum, frame_sum, c->Tg * sizeof(double), kind, c->stream), "sums");
+        if (frame_max != c->frame_max)
+            ck(cudaMemcpyAsync(c->frame_max, frame_max, c->Tg * sizeof(float), kind, c->stream), "max");
         const int mode_next = iter >= p->binarize_start ? 2 : 1;
         if (c->norms_cap < iter) {
             double* nn = nullptr;
@@ -2773,9 +2784,9 @@ int sfseg_shard_finalize(sfseg_ctx* c, const sfseg_params* p, int32_t iter,
             c->norms = nn;
             c->norms_cap = cap;
         }
-        sfk::k_finalize_total<<<1, sfk::kAuxThreads, 0, c->stream>>>(
-            c->frame_sum, c->frame_max, c->Tg, c->st, c->norms, iter - 1, mode_next,
-            lambda_for(p, iter), p->threshold_frac);
+        launch_pdl(sfk::k_finalize_total, 1, sfk::kAuxThreads, 0, c->stream,
+                   static_cast<const double*>(c->frame_sum), c->frame_max, c->Tg, c->st, c->norms,
+                   iter - 1, mode_next, lambda_for(p, iter), p->threshold_frac);
         launched(c->stream, "k_finalize_total");
         if (norm) {
             const IterState s = get_state(c, c->st);

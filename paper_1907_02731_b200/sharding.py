@@ -251,11 +251,13 @@ class ShardedSolver:
     def __init__(self, backend, rank: int, world: int, group=None):
         self.b = backend
         self.rank, self.world, self.group = rank, world, group
+        self._graphs = {}  # params -> "seen" | "eager" | (CUDAGraph, kept tensors)
 
     def load(self, T, H, W, S_local, F_local, x0_local, halo, allow_negative_affinity=False):
         """allow_negative_affinity must match the SfsegConfig the solve runs
         with (run() checks): off, the channels get the unit-range guard."""
         self.T, self.H, self.W, self.halo = T, H, W, halo
+        self._graphs = {}  # captured loops point at the previous problem's buffers
         self.t0, self.t1 = shard_range(T, self.world, self.rank)
         self.allow_negative = bool(allow_negative_affinity)
         if not self.allow_negative:
@@ -359,14 +361,10 @@ class ShardedSolver:
             raise ParameterError("allow_negative_affinity differs from the one the channels were "
                                  "loaded with (the unit-range guard is applied at load)")
 
-    def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
-        """out: optional preallocated host (soft, mask) arrays for this rank's
-        frames (the download lands there)."""
-        import torch
-
-        self._check_cfg(cfg)
-        params = cfg.to_params()
-        self.b.cfg = cfg
+    def _iterate(self, cfg, params) -> None:
+        """Enqueues iterations 1..cfg.iterations: step (halos pushed to the
+        peers by the kernel), one all-gather of the per-frame partials,
+        finalize. No host synchronisation."""
         for it in range(1, cfg.iterations + 1):
             io = self.b.step(params, it)
             self.b.before_exchange()
@@ -374,6 +372,65 @@ class ShardedSolver:
             fs, fm = self._gather_sums(io.frame_sum, io.frame_max)
             self.b.after_exchange()
             self.b.finalize(params, it, fs, fm)
+
+    def _graphable(self) -> bool:
+        """The whole loop can be captured into one CUDA graph when nothing in
+        it touches the host: a real CudaBackend, halos by peer memory (or one
+        rank) and an NCCL (or no) all-gather. SFSEG_SHARD_GRAPH=0 turns it off."""
+        import torch.distributed as dist
+
+        if os.environ.get("SFSEG_SHARD_GRAPH", "1") == "0" or not hasattr(self.b, "stream"):
+            return False
+        if self.world == 1:
+            return True
+        return self.p2p and dist.is_initialized() and dist.get_backend(self.group) == "nccl"
+
+    def _solve(self, cfg) -> None:
+        """One solve. The first solve of a loaded problem with a configuration
+        runs the loop eagerly (it also builds every lazily allocated buffer).
+        The second captures the same loop — kernels, peer pushes, the NCCL
+        all-gather — into a CUDA graph on the library's stream and replays it,
+        as does every later one: no per-iteration host work at all. A load
+        followed by a single solve (the end-to-end call) never pays a capture."""
+        import torch
+
+        self._check_cfg(cfg)
+        params = cfg.to_params()
+        self.b.cfg = cfg
+        key = bytes(params)
+        state = self._graphs.get(key) if self._graphable() else "eager"
+        if state is None:
+            self._graphs[key] = "seen"
+            state = "eager"
+        if state == "eager":
+            self._iterate(cfg, params)
+            return
+        if state == "seen":
+            self.b.ctx.synchronize()
+            kept = len(self.b._keep_gathered)
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.b.stream):
+                    self._iterate(cfg, params)  # recorded, not run
+            except Exception:
+                # capture refused (a backend or library call that cannot be
+                # captured): stay eager for good
+                torch.cuda.synchronize()
+                del self.b._keep_gathered[kept:]
+                self._graphs[key] = "eager"
+                self._iterate(cfg, params)
+                return
+            # the gathered tensors live in the graph's pool: keep them with it
+            state = (g, self.b._keep_gathered[kept:])
+            del self.b._keep_gathered[kept:]
+            self._graphs[key] = state
+        with torch.cuda.stream(self.b.stream):
+            state[0].replay()
+
+    def run(self, cfg, out=None) -> Tuple[np.ndarray, np.ndarray, List[float]]:
+        """out: optional preallocated host (soft, mask) arrays for this rank's
+        frames (the download lands there)."""
+        self._solve(cfg)
         norms = self.b.norms(cfg.iterations)
         if out is not None:
             soft, mask = self.b.download(cfg.final_threshold, self.t0, self.t1, out=out)
@@ -383,13 +440,4 @@ class ShardedSolver:
 
     def solve_only(self, cfg) -> None:
         """The iteration loop without the download (benchmark timing)."""
-        self._check_cfg(cfg)
-        params = cfg.to_params()
-        self.b.cfg = cfg
-        for it in range(1, cfg.iterations + 1):
-            io = self.b.step(params, it)
-            self.b.before_exchange()
-            self._exchange(io)
-            fs, fm = self._gather_sums(io.frame_sum, io.frame_max)
-            self.b.after_exchange()
-            self.b.finalize(params, it, fs, fm)
+        self._solve(cfg)

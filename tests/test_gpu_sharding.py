@@ -113,3 +113,41 @@ def test_peer_memory_halo_push_matches_single_context(world, arith, idx):
     for be, _, _ in ranks:
         be.set_peers(None, None)
         be.close()
+
+
+@pytest.mark.parametrize("arith,idx,binarize", [("fast", 1, False), ("exact", 1, True), ("fast", 2, False)])
+def test_sharded_driver_graph_replay_matches_eager(arith, idx, binarize):
+    # ShardedSolver captures its iteration loop into a CUDA graph on the
+    # second solve and replays it afterwards (no per-iteration host work):
+    # eager, capture + replay and replay must give the single-context bits,
+    # and a second configuration gets its own graph
+    from paper_1907_02731_b200.sharding import ShardedSolver
+
+    prob = synth.config(idx, frames=10)[0]
+    fs, _ = prob.generate()
+    if idx != 1:
+        fs = E.FeatureSet(np.ascontiguousarray(fs.unary[:, :100, :150]),
+                          [np.ascontiguousarray(f[:, :100, :150]) for f in fs.pairwise])
+    T, H, W = fs.unary.shape
+    base = {**prob.cfg.__dict__, "arith": arith, "binarize_start": 3 if binarize else 99}
+    cfgs = [E.SfsegConfig(**{**base, "iterations": 5}), E.SfsegConfig(**{**base, "iterations": 4})]
+    be = CudaBackend(0)
+    solver = ShardedSolver(be, 0, 1)
+    try:
+        solver.load(T, H, W, fs.unary, fs.pairwise, None, cfgs[0].kernel.radii[0])
+        for cfg in cfgs:
+            ref = E.run(fs, cfg)
+            for call in range(4):  # eager, capture + replay, replay, replay
+                soft, mask, norms = solver.run(cfg)
+                assert np.array_equal(soft, ref.soft), (cfg.iterations, call)
+                assert np.array_equal(mask, ref.mask)
+                assert np.array_equal(norms, [r.l2_norm_pre_normalize for r in ref.trace.iterations])
+        kinds = [type(v).__name__ for v in solver._graphs.values()]
+        assert kinds == ["tuple", "tuple"], kinds  # both loops were captured
+        # a reload drops the graphs (they point at the old buffers)
+        solver.load(T, H, W, fs.unary, fs.pairwise, None, cfgs[0].kernel.radii[0])
+        assert solver._graphs == {}
+        soft, _, _ = solver.run(cfgs[0])
+        assert np.array_equal(soft, E.run(fs, cfgs[0]).soft)
+    finally:
+        be.close()
