@@ -172,6 +172,17 @@ int sfref_convolve_separable(uint32_t T, uint32_t H, uint32_t W, const float* v,
     REF_CATCH
 }
 
+int sfref_convolve_direct(uint32_t T, uint32_t H, uint32_t W, const float* v,
+                          const int32_t radii[3], const double sigmas[3], float* out) {
+    REF_TRY
+    const auto k = sfseg::make_gaussian_kernel({sigmas[0], sigmas[1], sigmas[2]},
+                                               {radii[0], radii[1], radii[2]});
+    const auto r = sfseg::convolve_direct(vol(T, H, W, v, sfseg::VolumeRole::generic), k);
+    std::memcpy(out, r.data(), r.size() * sizeof(float));
+    return 0;
+    REF_CATCH
+}
+
 int sfref_step(uint32_t T, uint32_t H, uint32_t W, int32_t C, const float* x, const float* S,
                const float* const* F, const sfseg_params* p, int threads, float* out) {
     REF_TRY

@@ -39,7 +39,7 @@ from ._native import (CapacityError, CorruptionError, DegenerateSolutionError, E
 
 __all__ = [
     "KernelConfig", "SfsegConfig", "FeatureSet", "IterationRecord", "RunTrace", "RunResult",
-    "SeparableKernel3D", "make_gaussian_kernel", "convolve_separable", "sfseg_step",
+    "SeparableKernel3D", "make_gaussian_kernel", "convolve_separable", "convolve_direct", "sfseg_step",
     "sfseg_step_channel", "normalize_l2", "project_binary", "threshold_final", "run",
     "run_once", "run_batch",
     "separable_convolution_count", "Context", "default_context", "Error", "ParameterError",
@@ -297,6 +297,27 @@ def convolve_separable(v, kernel: KernelConfig | SeparableKernel3D, threads: int
     s = (C.c_double * 3)(*[float(x) for x in kernel.sigmas])
     with ctx.lock:
         N.check(ctx._lib.sfseg_convolve_separable(ctx.handle, T, H, W, b.ptr, r, s, ob.ptr, b.mem))
+    return out
+
+
+def convolve_direct(v, kernel: KernelConfig | SeparableKernel3D, ctx: Optional[Context] = None):
+    """convolve_direct (conv3d.cpp:187-243): the dense (2rt+1)(2ry+1)(2rx+1)
+    triple sum in fp64 with the reference's weight products and summation
+    order, cast to float — the check convolve_separable is tested against
+    (test_conv3d.cpp:159-176)."""
+    ctx = ctx or default_context()
+    k = kernel if isinstance(kernel, SeparableKernel3D) else make_gaussian_kernel(kernel.sigmas,
+                                                                                  kernel.radii)
+    b = _Buf(v)
+    T, H, W = _shape3(b.shape)
+    out = _empty_like(b)
+    ob = _Buf(out, writable=True)
+    r = (C.c_int32 * 3)(*[int(x) for x in k.radii])
+    tt, ty, tx = (np.ascontiguousarray(a, np.float64) for a in (k.taps_t, k.taps_y, k.taps_x))
+    with ctx.lock:
+        N.check(ctx._lib.sfseg_convolve_direct_taps(
+            ctx.handle, T, H, W, b.ptr, r, C.c_void_p(tt.ctypes.data), C.c_void_p(ty.ctypes.data),
+            C.c_void_p(tx.ctypes.data), ob.ptr, b.mem))
     return out
 
 

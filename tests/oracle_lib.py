@@ -150,6 +150,15 @@ class Reference(_Base):
             (C.c_double * 3)(*sigmas), C.c_int(threads), _vp(out)))
         return out
 
+
+    def convolve_direct(self, v, radii, sigmas):
+        v = np.ascontiguousarray(v, _F)
+        out = np.empty_like(v)
+        T, H, W = v.shape
+        self._chk(self.lib.sfref_convolve_direct(
+            C.c_uint32(T), C.c_uint32(H), C.c_uint32(W), _vp(v), (C.c_int32 * 3)(*radii),
+            (C.c_double * 3)(*sigmas), _vp(out)))
+        return out
     def step(self, x, S, F, cfg, threads=1):
         x, S = np.ascontiguousarray(x, _F), np.ascontiguousarray(S, _F)
         F = [np.ascontiguousarray(f, _F) for f in F]

@@ -316,3 +316,35 @@ def test_observer_may_call_the_engine_on_the_same_context(arith):
     # the observer's step of iterate k is the solve's step k+1: same norm
     norms = [r.l2_norm_pre_normalize for r in res.trace.iterations]
     assert np.allclose(seen[:-1], norms[1:], rtol=1e-5)
+
+
+@pytest.mark.parametrize("shape,radii,sigmas", [
+    ((5, 9, 11), (1, 2, 3), (0.5, 1.5, 1.5)),
+    ((3, 17, 40), (2, 4, 4), (0.7, 1.1, 2.0)),
+    ((6, 6, 6), (0, 1, 0), (1.0, 1e30, 1.0)),
+])
+def test_convolve_direct_matches_reference_and_separable(shape, radii, sigmas):
+    # conv3d.hpp:62-68 / conv3d.cpp:187-243: the dense fp64 triple sum. Bit
+    # for bit against the reference's own convolve_direct; and the relation
+    # test_conv3d.cpp:159-176 pins: separable == direct within 1e-5
+    v = random_volume(shape, 77)
+    k = E.KernelConfig(radii, sigmas)
+    got = E.convolve_direct(v, k)
+    sep = E.convolve_separable(v, k)
+    assert np.max(np.abs(got - sep)) <= 1e-5
+    if reference_available():
+        want = Reference().convolve_direct(v, radii, sigmas)
+        assert _equal_values(got, want), f"max diff {np.max(np.abs(got - want)):.3e}"
+    # impulse response = outer product of the taps (test_conv3d.cpp:110-139)
+    imp = np.zeros(shape, np.float32)
+    c = tuple(s // 2 for s in shape)
+    imp[c] = 1.0
+    kk = E.make_gaussian_kernel(sigmas, radii)
+    out = E.convolve_direct(imp, kk)
+    for dt in range(-radii[0], radii[0] + 1):
+        for dy in range(-radii[1], radii[1] + 1):
+            for dx in range(-radii[2], radii[2] + 1):
+                p = (c[0] + dt, c[1] + dy, c[2] + dx)
+                if all(0 <= p[a] < shape[a] for a in range(3)):
+                    w = kk.taps_t[dt + radii[0]] * kk.taps_y[dy + radii[1]] * kk.taps_x[dx + radii[2]]
+                    assert abs(float(out[p]) - w) <= 1e-6 * max(1.0, abs(w))
