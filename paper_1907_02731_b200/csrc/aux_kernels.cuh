@@ -122,6 +122,7 @@ __global__ void k_sq_acc(Vol q, Vol f, int first) {
 // launch (write_u) is the same S^p * y.
 __global__ void k_make_u(Vol xv, Vol sp, Vol u, const IterState* __restrict__ st) {
     griddep_wait();  // PDL: the previous finalize wrote st
+    if (st->stop) return;  // sfseg_solve_until already stopped
     const bool sig = st->mode == 2;
     const IterState s = *st;
     SFK_FOR_VOXELS(u, t, y, x) {
@@ -309,6 +310,7 @@ __global__ void k_finalize(const double* part, int per_frame, double* frame_sum,
     __shared__ double s[kAuxThreads];
     __shared__ bool is_last;
     griddep_wait();  // PDL: the step's partials are complete
+    if (st->stop) return;  // sfseg_solve_until already stopped: the state stays as it is
     const int t = blockIdx.x;
     const double* p = part + static_cast<size_t>(t) * per_frame;
     double acc = 0.0;
@@ -437,6 +439,7 @@ __device__ __forceinline__ float project_state(float a, const IterState& st) {
 __global__ void k_conv_stats(Vol cur, const IterState* st_cur, Vol prev, const IterState* st_prev,
                              int prev_raw, double* part) {
     __shared__ double s[4][kAuxThreads];
+    if (st_cur->stop) return;  // already stopped: nothing new to compare
     const IterState sc = *st_cur;
     const IterState sp = *st_prev;
     double d = 0.0, na = 0.0, nb = 0.0, df = 0.0;
@@ -462,13 +465,37 @@ __global__ void k_conv_stats(Vol cur, const IterState* st_cur, Vol prev, const I
     if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_conv_final(const double* part, int nblocks, double* out4) {
+// The stopping rule itself, on the device: criterion 0 is ||x_k - x_{k-1}||_2 <
+// tol (oracle.cpp:234-242), 1 is angle(x_k, x_{k-1}) < tol degrees
+// (bench.cpp:75-80, metrics.cpp:22-38). When it holds, st->stop = iter and the
+// kernels of the later iterations already in the stream do nothing; the host
+// reads the state back once per chunk of iterations, not once per iteration.
+__global__ void k_conv_final(const double* part, int nblocks, double* out4, IterState* st, int iter,
+                             int criterion, double tol) {
+    __shared__ double h[4];
+    if (st->stop) return;
     if (threadIdx.x < 4) {
         double acc = 0.0;
         for (int b = 0; b < nblocks; ++b) acc += part[b * 4 + threadIdx.x];
         out4[threadIdx.x] = acc;
+        h[threadIdx.x] = acc;
     }
+    __syncthreads();
+    if (threadIdx.x != 0 || st->degenerate) return;
+    bool stop;
+    if (criterion == 0) {
+        stop = sqrt(h[3]) < tol;
+    } else if (h[1] == 0.0 || h[2] == 0.0) {
+        st->stop = -iter;  // angle of a zero vector
+        return;
+    } else {
+        const double cs = fmin(1.0, fmax(-1.0, h[0] / (sqrt(h[1]) * sqrt(h[2]))));
+        stop = acos(cs) * 57.295779513082320876798154814105 < tol;
+    }
+    if (stop) st->stop = iter;
 }
+
+__global__ void k_clear_stop(IterState* st) { st->stop = 0; }
 
 // ---- generic (any-radius) stencil: conv3d.cpp:80-167 on pitched volumes --
 

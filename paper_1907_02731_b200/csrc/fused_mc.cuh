@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 
     const int tid = threadIdx.x;
     griddep_wait();  // PDL: the previous step / finalize has completed
-    if (a.st->degenerate) return;  // an earlier iteration hit a zero norm
+    // an earlier iteration hit a zero norm, or the early-exit rule already held
+    if (a.st->degenerate || a.st->stop) return;
     const int s0 = a.sched_off[blockIdx.x], s1 = a.sched_off[blockIdx.x + 1];
     if (s0 >= s1) return;
 

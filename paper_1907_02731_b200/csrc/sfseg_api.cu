@@ -1354,9 +1354,13 @@ void solve_impl(sfseg_ctx* c, const sfseg_params* p, int first, int last,
 // run() always runs cfg.iterations; power_iteration stops once
 // ||x_k - x_{k-1}||_2 < tol (oracle.cpp:234-242) and bench.cpp's
 // converged_conv once angle(x_k, x_{k-1}) < tol degrees (bench.cpp:75-80,
-// metrics.cpp:22-38). Each iteration here is the same fused step + finalize
-// as solve_impl, then k_conv_stats against the previous projected iterate and
-// one 32-byte read-back for the host's test.
+// metrics.cpp:22-38). Each iteration is the same fused step + finalize as
+// solve_impl, then k_conv_stats against the previous projected iterate and
+// k_conv_final, which evaluates the rule ON THE DEVICE and raises the state's
+// stop flag; the kernels of later iterations already in the stream see the
+// flag and return, so the iterate stays at the stopping iteration. Iterations
+// are enqueued in chunks and the host reads the flag back once per chunk: no
+// host round trip per iteration.
 void solve_until_impl(sfseg_ctx* c, const sfseg_params* p, int first, int max_iter, int criterion,
                       double tol, int32_t* done, sfseg_iter_record* rec) {
     if (criterion != SFSEG_CONV_STEP && criterion != SFSEG_CONV_ANGLE)
@@ -1366,40 +1370,93 @@ void solve_until_impl(sfseg_ctx* c, const sfseg_params* p, int first, int max_it
     if (!c->resident) fail(SFSEG_ERR_STATE, "sfseg_solve_until before sfseg_load");
     if (first < 1 || max_iter < first) fail(SFSEG_ERR_PARAMETER, "bad iteration range");
     if (first > 1 && c->cur < 0) fail(SFSEG_ERR_STATE, "continuing a solve that never started");
+    const HostKernel k = make_kernel(p->radii, p->sigmas);
+    ensure_guard(c, !p->allow_negative_affinity);
+    ensure_sp(c, p->p);
     const int nb = aux_grid(c);
     if (!c->conv_part) {
         ck(cudaMalloc(&c->conv_part, (static_cast<size_t>(nb) * 4 + 4) * sizeof(double)), "malloc");
         ck(cudaMalloc(&c->st_prev, sizeof(IterState)), "malloc");
     }
-    int it = first;
-    for (; it <= max_iter; ++it) {
-        // x_{k-1}: the visible iterate before this step
-        const bool prev_raw = c->cur < 0;
-        const float* prev = prev_raw ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
-        ck(cudaMemcpyAsync(c->st_prev, c->st, sizeof(IterState), cudaMemcpyDeviceToDevice, c->stream),
-           "state copy");
-        sfseg_iter_record r{};
-        solve_impl(c, p, it, it, rec ? &r : nullptr);  // syncs; throws on a zero norm
-        if (rec) rec[it - first] = r;
-        sfk::k_conv_stats<<<nb, sfk::kAuxThreads, 0, c->stream>>>(
-            c->vol(c->y[c->cur]), c->st, c->vol(const_cast<float*>(prev)), c->st_prev, prev_raw,
-            c->conv_part);
-        sfk::k_conv_final<<<1, 32, 0, c->stream>>>(c->conv_part, nb, c->conv_part + 4 * nb);
-        launched(c->stream, "k_conv_stats");
-        double h[4];
-        ck(cudaMemcpyAsync(h, c->conv_part + 4 * nb, sizeof h, cudaMemcpyDeviceToHost, c->stream), "D2H");
-        ck(cudaStreamSynchronize(c->stream), "sync");
-        bool stop;
-        if (criterion == SFSEG_CONV_STEP) {
-            stop = std::sqrt(h[3]) < tol;
-        } else {
-            if (h[1] == 0.0 || h[2] == 0.0) fail(SFSEG_ERR_PARAMETER, "angle is undefined for a zero vector");
-            const double cs = std::clamp(h[0] / (std::sqrt(h[1]) * std::sqrt(h[2])), -1.0, 1.0);
-            stop = std::acos(cs) * 57.295779513082320876798154814105 < tol;
-        }
-        if (stop) break;
+    const int nmax = max_iter - first + 1;
+    if (c->norms_cap < nmax) {
+        if (c->norms) cudaFree(c->norms);
+        c->norms = nullptr;
+        c->norms_cap = 0;
+        ck(cudaMalloc(&c->norms, nmax * sizeof(double)), "cudaMalloc norms");
+        c->norms_cap = nmax;
     }
-    *done = std::min(it, max_iter);
+    if (first == 1) {
+        IterState s{};
+        s.mode = 0;
+        set_state(c, c->st, s);
+        ck(cudaMemsetAsync(c->frame_max, 0, c->Tout() * sizeof(float), c->stream), "memset");
+        c->cur = -1;
+        c->cur_u = false;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, c->stream), "event");
+    constexpr int kChunk = 8;  // iterations per flag read-back
+    std::vector<int> cur_after(nmax, -1);  // y index holding the iterate after iteration first + i
+    int it = first, stop = 0;
+    while (it <= max_iter && stop == 0) {
+        const int chunk_end = std::min(max_iter, it + kChunk - 1);
+        for (; it <= chunk_end; ++it) {
+            // x_{k-1}: the visible iterate before this step
+            const bool prev_raw = c->cur < 0;
+            const float* prev = prev_raw ? (c->has_x0 ? c->x0 : c->S) : c->y[c->cur];
+            const int dst = c->cur < 0 ? 0 : 1 - c->cur;
+            ck(cudaMemcpyAsync(c->st_prev, c->st, sizeof(IterState), cudaMemcpyDeviceToDevice, c->stream),
+               "state copy");
+            // every iteration may be the last one: the iterate stays y (no U carry)
+            c->cur_u = launch_step(c, k, p->alpha, prev, c->st, c->y[dst], c->Fw,
+                                   p->arith == SFSEG_ARITH_FAST, c->cur >= 0 && c->cur_u, false);
+            const int mode_next = it >= p->binarize_start ? 2 : 1;
+            finalize(c, c->st, c->norms, it - first, mode_next, lambda_for(p, it), p->threshold_frac);
+            c->cur = dst;
+            cur_after[it - first] = dst;
+            sfk::k_conv_stats<<<nb, sfk::kAuxThreads, 0, c->stream>>>(
+                c->vol(c->y[dst]), c->st, c->vol(const_cast<float*>(prev)), c->st_prev, prev_raw,
+                c->conv_part);
+            sfk::k_conv_final<<<1, 32, 0, c->stream>>>(c->conv_part, nb, c->conv_part + 4 * nb, c->st,
+                                                       it, criterion, tol);
+            launched(c->stream, "k_conv_stats");
+        }
+        stop = get_state(c, c->st).stop;  // one read-back (and sync) per chunk
+    }
+    ck(cudaEventRecord(e1, c->stream), "event");
+    const int last = stop != 0 ? std::abs(stop) : max_iter;  // last iteration that really ran
+    const int n = last - first + 1;
+    std::vector<double> norms(n);
+    ck(cudaMemcpyAsync(norms.data(), c->norms, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+       "norms");
+    sfk::k_clear_stop<<<1, 1, 0, c->stream>>>(c->st);
+    launched(c->stream, "k_clear_stop");
+    ck(cudaStreamSynchronize(c->stream), "solve_until");
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // the host's view of the iterate: what iteration `last` wrote
+    c->cur = cur_after[n - 1];
+    c->cur_u = false;
+    sfseg_timing tm{};
+    tm.solve_ms = ms;
+    c->last_timing = tm;
+    if (rec)
+        for (int i = 0; i < n; ++i) {
+            rec[i].iter = first + i;
+            rec[i].l2_norm_pre_normalize = norms[i];
+            rec[i].angle_deg = NAN;
+            rec[i].iou = NAN;
+            rec[i].wall_time_s = ms * 1e-3 / std::max(1, it - first);  // mean over the enqueued iterations
+        }
+    *done = last;
+    for (int i = 0; i < n; ++i)
+        if (norms[i] == 0.0) fail(SFSEG_ERR_DEGENERATE, "iterate collapsed to the zero vector");
+    if (stop < 0) fail(SFSEG_ERR_PARAMETER, "angle is undefined for a zero vector");
 }
 
 // The copy stream and the two-slot staging ring of pipelined host transfers;

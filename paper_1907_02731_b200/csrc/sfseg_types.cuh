@@ -22,6 +22,11 @@ struct IterState {
     float max_raw;     // max(0, max y_k)
     float max_unit;    // max(0, max x_unit)
     float inv_f, theta_f, lambda_f;  // float copies for the FAST arithmetic
+    // sfseg_solve_until: set on the device by k_conv_final once the stopping
+    // rule holds (> 0: the iteration it held at; < 0: the rule is undefined, a
+    // zero vector). While it is set, every kernel of the later iterations
+    // already in the stream returns at once, so the iterate stays put.
+    int32_t stop;
 };
 
 // Arguments of one fused stencil launch (one channel group of one step).

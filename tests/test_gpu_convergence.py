@@ -68,3 +68,57 @@ def test_zero_tolerance_runs_every_iteration_like_run():
     full = E.run(fs, cfg)
     assert np.array_equal(res.soft, full.soft)
     assert np.array_equal(res.mask, full.mask)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_stop_is_decided_on_the_device_and_the_solve_resumes(arith):
+    # the stopping rule is evaluated by k_conv_final on the device: iterations
+    # already enqueued behind the stopping one must leave the iterate alone,
+    # and a later sfseg_solve continues from it exactly as a straight
+    # fixed-count solve would
+    import ctypes as C
+
+    from paper_1907_02731_b200 import _native as N
+
+    prob = synth.config(0)[0]
+    fs, _ = prob.generate()
+    cfg = E.SfsegConfig(**{**prob.cfg.__dict__, "arith": arith, "iterations": 400,
+                           "binarize_start": 401})
+    p = cfg.to_params()
+    ctx = E.Context(0)
+    lib = ctx._lib
+    try:
+        T, H, W = fs.unary.shape
+        fp = (C.c_void_p * 1)(fs.pairwise[0].ctypes.data)
+        load = lambda: N.check(lib.sfseg_load(ctx.handle, T, H, W, 1, C.c_void_p(fs.unary.ctypes.data),
+                                              C.cast(fp, C.c_void_p), None, N.SFSEG_MEM_HOST))
+        soft = lambda: (lambda a: (N.check(lib.sfseg_download(ctx.handle, 0.5, C.c_void_p(a.ctypes.data),
+                                                              None, N.SFSEG_MEM_HOST)), a)[1])(
+            np.empty(fs.unary.shape, np.float32))
+        load()
+        done = C.c_int32()
+        recs = (N.IterRecord * 400)()
+        N.check(lib.sfseg_solve_until(ctx.handle, C.byref(p), 1, 400, N.SFSEG_CONV_STEP, 1e-5,
+                                      C.byref(done), recs))
+        k = done.value
+        assert 3 < k < 392  # iterations k+1.. of its chunk were already enqueued when it stopped
+        x_stop = soft()
+        # a straight k-iteration solve gives the same iterate bit for bit: the
+        # iterations enqueued after the stopping one did nothing
+        load()
+        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), 1, k, None))
+        assert np.array_equal(soft(), x_stop)
+        # and the stopped solve resumes (the flag was cleared)
+        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), k + 1, k + 2, None))
+        x_more = soft()
+        load()
+        N.check(lib.sfseg_solve_until(ctx.handle, C.byref(p), 1, 400, N.SFSEG_CONV_STEP, 1e-5,
+                                      C.byref(done), recs))
+        assert done.value == k
+        N.check(lib.sfseg_solve(ctx.handle, C.byref(p), k + 1, k + 2, None))
+        assert np.array_equal(soft(), x_more)
+        assert not np.array_equal(x_more, x_stop)
+        assert [recs[i].iter for i in range(k)] == list(range(1, k + 1))
+        assert all(recs[i].l2_norm_pre_normalize > 0 for i in range(k))
+    finally:
+        ctx.close()
