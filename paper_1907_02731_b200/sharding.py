@@ -376,14 +376,19 @@ class ShardedSolver:
     def _graphable(self) -> bool:
         """The whole loop can be captured into one CUDA graph when nothing in
         it touches the host: a real CudaBackend, halos by peer memory (or one
-        rank) and an NCCL (or no) all-gather. SFSEG_SHARD_GRAPH=0 turns it off."""
+        rank) and an NCCL (or no) all-gather. One rank: on by default
+        (SFSEG_SHARD_GRAPH=0 turns it off). Several ranks: the capture then
+        includes the NCCL all-gather, which could only be exercised on
+        single-GPU boxes so far, so it is opt-in (SFSEG_SHARD_GRAPH=1)."""
         import torch.distributed as dist
 
-        if os.environ.get("SFSEG_SHARD_GRAPH", "1") == "0" or not hasattr(self.b, "stream"):
+        env = os.environ.get("SFSEG_SHARD_GRAPH", "")
+        if env == "0" or not hasattr(self.b, "stream"):
             return False
         if self.world == 1:
             return True
-        return self.p2p and dist.is_initialized() and dist.get_backend(self.group) == "nccl"
+        return (env == "1" and self.p2p and dist.is_initialized()
+                and dist.get_backend(self.group) == "nccl")
 
     def _solve(self, cfg) -> None:
         """One solve. The first solve of a loaded problem with a configuration
@@ -410,7 +415,9 @@ class ShardedSolver:
             kept = len(self.b._keep_gathered)
             try:
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=self.b.stream):
+                # thread_local: another thread's CUDA calls (the NCCL watchdog's event
+                # queries) must not invalidate the capture
+                with torch.cuda.graph(g, stream=self.b.stream, capture_error_mode="thread_local"):
                     self._iterate(cfg, params)  # recorded, not run
             except Exception:
                 # capture refused (a backend or library call that cannot be
