@@ -145,3 +145,22 @@ def test_synth_frame_range_is_the_slab_of_the_whole_volume(idx, frames, rng):
     assert np.array_equal(part.unary, whole.unary[t0:t1])
     assert all(np.array_equal(a, b[t0:t1]) for a, b in zip(part.pairwise, whole.pairwise))
     assert np.array_equal(pm, m[t0:t1])
+
+
+def test_headers_are_plain_c99(tmp_path):
+    # the drop-in boundary is a C ABI: both headers must compile as C (no C++
+    # constructs, no torch / CUDA types in the signatures)
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        pytest.skip("no C compiler")
+    src = tmp_path / "hdr.c"
+    src.write_text('#include "sfseg_cuda.h"\n#include "sfseg_synth.h"\n'
+                   "int main(void) { sfseg_clip c; sfseg_params p; sfseg_iter_record r;\n"
+                   "  (void)c; (void)p; (void)r; return 0; }\n")
+    inc = N.CUDA_LIB.parents[2] / "include"
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only",
+                        f"-I{inc}", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
