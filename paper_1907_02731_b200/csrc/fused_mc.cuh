@@ -503,28 +503,34 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                     bulk_commit();
                 }
                 ++ecnt;
-                if (last) {
-                    // canonical reduction (device_common.cuh): 4-row blocks, fp32
-                    // column sums, xor-butterfly over the 32 columns
+                if (last) {  // launch-uniform: the earlier launches of a step skip it
+                    // canonical reduction (device_common.cuh): 4-row blocks, column
+                    // sums (fp32 in FAST, fp64 in EXACT as fused_ws.cuh), xor-butterfly
+                    // over the 32 columns. The warp's two blocks share one butterfly:
+                    // after the first exchange lanes 0-15 hold block 0's pair sums
+                    // c_i + c_{i+16} and lanes 16-31 block 1's — the values the
+                    // per-block xor-16 step leaves there — and the xor 8, 4, 2, 1
+                    // steps stay inside each half: same bits, half the shuffles.
+                    static_assert(BR == 8, "two 4-row blocks per warp");
+                    using RT_ = std::conditional_t<EXACT, double, float>;
+                    RT_ cs0 = 0, cs1 = 0;
 #pragma unroll
-                    for (int h = 0; h < BR / 4; ++h) {
-                        // EXACT: fp64 column sums and butterfly (fused_ws.cuh)
-                        using RT_ = std::conditional_t<EXACT, double, float>;
-                        RT_ cs = 0;
-#pragma unroll
-                        for (int r = 0; r < 4; ++r)
-                            cs += static_cast<RT_>(v[4 * h + r]) * static_cast<RT_>(v[4 * h + r]);
-#pragma unroll
-                        for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-                        const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + h;
-                        if (lane == 0 && gb < a.nbands && q.tile_x < a.nhalves)
-                            a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
-                                static_cast<double>(cs);
+                    for (int r = 0; r < 4; ++r) {
+                        cs0 += static_cast<RT_>(v[r]) * static_cast<RT_>(v[r]);
+                        cs1 += static_cast<RT_>(v[4 + r]) * static_cast<RT_>(v[4 + r]);
                     }
+                    const bool lo = lane < 16;
+                    RT_ cs = (lo ? cs0 : cs1) + __shfl_xor_sync(0xffffffffu, lo ? cs1 : cs0, 16);
+#pragma unroll
+                    for (int o = 8; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
                     float cmax = 0.0f;
 #pragma unroll
                     for (int r = 0; r < BR; ++r) cmax = fmaxf(cmax, v[r]);
                     const int wm = __reduce_max_sync(0xffffffffu, __float_as_int(cmax));
+                    const int gb = q.tile_y * G::NBANDS + (BR / 4) * wb + (lo ? 0 : 1);
+                    if ((lane & 15) == 0 && gb < a.nbands && q.tile_x < a.nhalves)
+                        a.part[(static_cast<size_t>(to - a.part_t0) * a.nbands + gb) * a.nhalves + q.tile_x] =
+                            static_cast<double>(cs);
                     if (lane == 0) atomic_max_nonneg(a.frame_max + (to - a.part_t0), __int_as_float(wm));
                 }
             }
