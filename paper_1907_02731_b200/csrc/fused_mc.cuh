@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
     uint64_t* slab_full = mbar + STAGES + 2 * NXB;  // [NWB]
 
     __shared__ IterState st;
-    __shared__ PlaneStream slabq[NWB];
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x;
@@ -351,27 +350,26 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
 
         float* slab = bsl + static_cast<size_t>(wb) * (NOP + 1) * SLAB;
         uint64_t* sfull = &slab_full[wb];
-        PlaneStream& eq = slabq[wb];  // lane 0 only
-        auto issue_slab = [&]() {
-            if (eq.done) return;
+        // operands of output plane `tout` (global frame) of tile (tx, ty)
+        auto issue_slab = [&](int tx, int ty, int tout) {
             const bool yprev = !HEAD && !(EXACT && first);
             mbar_arrive_expect_tx(sfull, (yprev ? NOP : NOP - (HEAD ? 0 : 1)) * SLAB * sizeof(float));
-            const int x = eq.tile_x * TX, y = eq.tile_y * TY + BR * wb, t = a.out_t0 + eq.p - a.buf_t0;
+            const int x = tx * TX, y = ty * TY + BR * wb, t = tout - a.buf_t0;
             tma_load_3d(slab, &a.tm_spc, sfull, x, y, t);
 #pragma unroll
             for (int i = 0; i < G::NFC; ++i)
                 tma_load_3d(slab + (1 + i) * SLAB, &a.tm_fc[i], sfull, x, y, t);
             if (yprev)  // y so far: written by the previous launch (stream order)
                 tma_load_3d(slab + (NOP - 1) * SLAB, &a.tm_out, sfull, x, y, t + a.buf_t0 - a.out_buf_t0);
-            eq.next();
         };
-        if (lane == 0) {
-            eq.init(a.sched + s0, s1 - s0, 0, a.tiles_x);
-            issue_slab();
-        }
 
         PlaneStream q;
         q.init(a.sched + s0, s1 - s0, RT, a.tiles_x);
+        // the first output plane's operands; every emitted plane then fetches
+        // the next one's: the following frame of the segment, or the first
+        // frame of the next segment (no second plane cursor: the issue sits on
+        // every B warp's chain)
+        if (lane == 0 && !q.done) issue_slab(q.tile_x, q.tile_y, a.out_t0 + q.ta);
         int cnt = 0, ecnt = 0, rslot = 0;
         while (!q.done) {
             const int tg = a.out_t0 + q.p;
@@ -459,7 +457,13 @@ __global__ void __launch_bounds__(McGeom<RT, R, NF, KIND>::NT, 1)
                 __syncwarp();
                 if (lane == 0) {
                     fence_proxy_async();  // the reads above before the next TMA write
-                    issue_slab();
+                    if (q.p + 1 < q.tb + RT) {
+                        issue_slab(q.tile_x, q.tile_y, to + 1);
+                    } else if (q.i + 1 < q.n) {
+                        const int4 sg = q.seg[q.i + 1];
+                        const int ny = sg.x / q.tiles_x;
+                        issue_slab(sg.x - ny * q.tiles_x, ny, a.out_t0 + sg.y);
+                    }
                 }
                 const int ox = q.tile_x * TX, oy = q.tile_y * TY + BR * wb;
                 float v[BR];
