@@ -273,15 +273,28 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
         // binarised iterations (mode 2) come normalised in U
         const float scale = st.mode == 1 ? st.inv_f : 1.0f;
 
-        constexpr int KR = TMR ? 1 : K;  // register ring depth
-        float2 ringu[BR / 2][KR];  // u of rows (2k, 2k+1)
-        float2 ringp[BR][KR];      // (F u, F^2 u) of row r
+        // t-pass in scatter form (register variants): instead of a ring of the
+        // last K y-filtered planes summed at emission, KA = K - 1 pending
+        // outputs are kept as running sums. Plane p completes output p - RT
+        // with its last tap (the only t-pass work between the y-pass and the
+        // recombination), starts output p + RT with tap 0 in the freed slot
+        // and adds to the K - 2 outputs in between; those updates have no
+        // consumer until later planes, so they sit in the epilogue's latency
+        // shadows. An output still receives taps 0..2RT in plane order: the
+        // same FMA sequence, the same bits as the gather form. A slot is
+        // re-initialised (tap 0) before its output's other taps arrive, so
+        // nothing carries over between schedule segments.
+        constexpr int KA = TMR ? 1 : K - 1;
+        static_assert(TMR || RT >= 1, "scatter t-pass needs a temporal radius");
+        float2 yu[BR / 2], yp[BR];  // y-filtered current plane: u of rows (2k, 2k+1); (F u, F^2 u) of row r
+        float2 accu[BR / 2][KA];
+        float2 accp[BR][KA];
 #pragma unroll
-        for (int k = 0; k < KR; ++k) {
+        for (int k = 0; k < KA; ++k) {
 #pragma unroll
-            for (int r = 0; r < BR / 2; ++r) ringu[r][k] = zero2;
+            for (int r = 0; r < BR / 2; ++r) accu[r][k] = zero2;
 #pragma unroll
-            for (int r = 0; r < BR; ++r) ringp[r][k] = zero2;
+            for (int r = 0; r < BR; ++r) accp[r][k] = zero2;
         }
         // TMEM ring: slot = 3 BR words (u pairs, then (F u, F^2 u) per row) in
         // this thread's TMEM lane; warps w and w + 4 share a lane quadrant
@@ -378,15 +391,14 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
         };
 
         auto plane = [&](auto slot_c) {
-            constexpr int S_ = decltype(slot_c)::value;
-            constexpr int SR = TMR ? 0 : S_;  // register slot of this plane
-            [[maybe_unused]] const int slot = TMR ? rslot : S_;
+            constexpr int S_ = decltype(slot_c)::value;  // register variants: the emitting slot
+            [[maybe_unused]] const int slot = rslot;     // TMEM ring: slot of this plane
             const int tg = a.out_t0 + q.p;
             const bool valid = tg >= 0 && tg < a.T;
             const bool emit = q.p - RT >= q.ta;
             const int to = tg - RT;
 
-            // y-pass (conv3d.cpp:113-135) into this plane's ring slot
+            // y-pass (conv3d.cpp:113-135) of this plane
             if (valid) {
                 const int b = cnt % NXB;
                 mbar_wait(&xb_full[b], (cnt / NXB) & 1);
@@ -407,27 +419,41 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                     for (int k = 0; k < BR / 2; ++k) {
                         const float vv = vin[2 * k + e];
                         if (e == 0)  // zero-partner edge taps as scalar ops
-                            ringu[k][SR] = make_float2(vv * a.taps_y[0], 0.0f);
+                            yu[k] = make_float2(vv * a.taps_y[0], 0.0f);
                         else if (e == 2 * R + 1)
-                            ringu[k][SR].y = fmaf(vv, a.taps_y[2 * R], ringu[k][SR].y);
+                            yu[k].y = fmaf(vv, a.taps_y[2 * R], yu[k].y);
                         else
-                            ringu[k][SR] = ffma2(make_float2(vv, vv), a.tpair_y[e], ringu[k][SR]);
+                            yu[k] = ffma2(make_float2(vv, vv), a.tpair_y[e], yu[k]);
                     }
                     if (e <= 2 * R) {
 #pragma unroll
                         for (int r = 0; r < BR; ++r)
-                            ringp[r][SR] = ffma2(pv[r + e], make_float2(a.taps_y[e], a.taps_y[e]),
-                                                 e == 0 ? zero2 : ringp[r][SR]);
+                            yp[r] = ffma2(pv[r + e], make_float2(a.taps_y[e], a.taps_y[e]), e == 0 ? zero2 : yp[r]);
                     }
                 }
                 mbar_arrive(&xb_empty[b]);
                 ++cnt;
             } else {
 #pragma unroll
-                for (int r = 0; r < BR / 2; ++r) ringu[r][SR] = zero2;
+                for (int r = 0; r < BR / 2; ++r) yu[r] = zero2;
 #pragma unroll
-                for (int r = 0; r < BR; ++r) ringp[r][SR] = zero2;
+                for (int r = 0; r < BR; ++r) yp[r] = zero2;
             }
+            // scatter step j of this plane (register variants): j = 0 starts
+            // the output RT planes ahead in the slot the emission freed, j >= 1
+            // adds tap K - 1 - j to the output emitted j planes from now
+            [[maybe_unused]] auto scatter = [&](auto jc) {
+                constexpr int J = decltype(jc)::value;
+                if constexpr (!TMR && J < KA) {
+                    constexpr int SJ = (S_ + J) % KA;
+                    const float2 w2 = make_float2(a.taps_t[J == 0 ? 0 : K - 1 - J], a.taps_t[J == 0 ? 0 : K - 1 - J]);
+#pragma unroll
+                    for (int k = 0; k < BR / 2; ++k) accu[k][SJ] = ffma2(yu[k], w2, J == 0 ? zero2 : accu[k][SJ]);
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) accp[r][SJ] = ffma2(yp[r], w2, J == 0 ? zero2 : accp[r][SJ]);
+                }
+            };
+            using std::integral_constant;
             if (emit) {
                 // t-pass (conv3d.cpp:147-165): oldest..newest take taps_t[0..2RT]
                 float2 tu[BR / 2], tp[BR];
@@ -439,9 +465,9 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                         float2 lu[BR / 2], lp[BR];
                         if (d == K - 1) {
 #pragma unroll
-                            for (int k = 0; k < BR / 2; ++k) lu[k] = ringu[k][0];
+                            for (int k = 0; k < BR / 2; ++k) lu[k] = yu[k];
 #pragma unroll
-                            for (int r = 0; r < BR; ++r) lp[r] = ringp[r][0];
+                            for (int r = 0; r < BR; ++r) lp[r] = yp[r];
                         } else {
                             ring_ld((slot + 1 + d) % K, lu, lp);
                         }
@@ -452,20 +478,12 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                         for (int r = 0; r < BR; ++r) tp[r] = ffma2(lp[r], w2, d == 0 ? zero2 : tp[r]);
                     }
                 } else {
+                    // the last tap completes the output in slot S_
+                    const float2 wl = make_float2(a.taps_t[K - 1], a.taps_t[K - 1]);
 #pragma unroll
-                    for (int k = 0; k < BR / 2; ++k) {
-                        tu[k] = ffma2(ringu[k][(S_ + 1) % K], make_float2(a.taps_t[0], a.taps_t[0]), zero2);
+                    for (int k = 0; k < BR / 2; ++k) tu[k] = ffma2(yu[k], wl, accu[k][S_]);
 #pragma unroll
-                        for (int d = 1; d < K; ++d)
-                            tu[k] = ffma2(ringu[k][(S_ + 1 + d) % K], make_float2(a.taps_t[d], a.taps_t[d]), tu[k]);
-                    }
-#pragma unroll
-                    for (int r = 0; r < BR; ++r) {
-                        tp[r] = ffma2(ringp[r][(S_ + 1) % K], make_float2(a.taps_t[0], a.taps_t[0]), zero2);
-#pragma unroll
-                        for (int d = 1; d < K; ++d)
-                            tp[r] = ffma2(ringp[r][(S_ + 1 + d) % K], make_float2(a.taps_t[d], a.taps_t[d]), tp[r]);
-                    }
+                    for (int r = 0; r < BR; ++r) tp[r] = ffma2(yp[r], wl, accp[r][S_]);
                 }
                 float spv[BR], fv[BR];
                 mbar_wait(sfull, ecnt & 1);
@@ -474,6 +492,8 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                     spv[r] = slab[r * TX + lane];
                     fv[r] = slab[SLSTEP + r * TX + lane];
                 }
+                scatter(integral_constant<int, 0>{});
+                scatter(integral_constant<int, 1>{});
                 if constexpr (WIDE) {
                     if (bt == 0) bulk_wait_read0();  // the previous y tile store has read the staging
                     named_bar_sync(3, NB);            // every B warp has read the tiles
@@ -498,6 +518,10 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                 }
                 const int ox = q.tile_x * TX, oy = q.tile_y * TY + BR * wb;
                 reduce_plane(v, to, q.tile_x, q.tile_y, last);
+                scatter(integral_constant<int, 2>{});
+                scatter(integral_constant<int, 3>{});
+                scatter(integral_constant<int, 4>{});
+                scatter(integral_constant<int, 5>{});
                 if constexpr (WIDE) {
                     float* ost = slab + 2 * SLSTEP;
 #pragma unroll
@@ -540,22 +564,30 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
                     }
                 }
                 ++ecnt;
+            } else {
+                // the first 2RT planes of a segment emit nothing
+                scatter(integral_constant<int, 0>{});
+                scatter(integral_constant<int, 1>{});
+                scatter(integral_constant<int, 2>{});
+                scatter(integral_constant<int, 3>{});
+                scatter(integral_constant<int, 4>{});
+                scatter(integral_constant<int, 5>{});
             }
             if constexpr (TMR) {
                 // this plane into its slot (it held a plane no longer needed)
                 float w[8];
 #pragma unroll
                 for (int k = 0; k < BR / 2; ++k) {
-                    w[2 * k] = ringu[k][0].x;
-                    w[2 * k + 1] = ringu[k][0].y;
+                    w[2 * k] = yu[k].x;
+                    w[2 * k + 1] = yu[k].y;
                 }
                 tmem_st8(tm_ring + slot * RW, w);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
-                        w[2 * r] = ringp[4 * h + r][0].x;
-                        w[2 * r + 1] = ringp[4 * h + r][0].y;
+                        w[2 * r] = yp[4 * h + r].x;
+                        w[2 * r + 1] = yp[4 * h + r].y;
                     }
                     tmem_st8(tm_ring + slot * RW + 8 + 8 * h, w);
                 }
@@ -567,14 +599,13 @@ __global__ void __launch_bounds__(RsGeom<RT, R, STAGES, TMR_>::NT, 1)
         if constexpr (TMR) {
             while (!q.done) plane(integral_constant<int, 0>{});  // runtime slots
         } else while (!q.done) {
-            // register ring: the slot index must be a compile-time constant
+            // pending-output slots: the index must be a compile-time constant
             plane(integral_constant<int, 0>{});
-            if constexpr (K > 1) { if (q.done) break; plane(integral_constant<int, (K > 1 ? 1 : 0)>{}); }
-            if constexpr (K > 2) { if (q.done) break; plane(integral_constant<int, (K > 2 ? 2 : 0)>{}); }
-            if constexpr (K > 3) { if (q.done) break; plane(integral_constant<int, (K > 3 ? 3 : 0)>{}); }
-            if constexpr (K > 4) { if (q.done) break; plane(integral_constant<int, (K > 4 ? 4 : 0)>{}); }
-            if constexpr (K > 5) { if (q.done) break; plane(integral_constant<int, (K > 5 ? 5 : 0)>{}); }
-            if constexpr (K > 6) { if (q.done) break; plane(integral_constant<int, (K > 6 ? 6 : 0)>{}); }
+            if constexpr (KA > 1) { if (q.done) break; plane(integral_constant<int, (KA > 1 ? 1 : 0)>{}); }
+            if constexpr (KA > 2) { if (q.done) break; plane(integral_constant<int, (KA > 2 ? 2 : 0)>{}); }
+            if constexpr (KA > 3) { if (q.done) break; plane(integral_constant<int, (KA > 3 ? 3 : 0)>{}); }
+            if constexpr (KA > 4) { if (q.done) break; plane(integral_constant<int, (KA > 4 ? 4 : 0)>{}); }
+            if constexpr (KA > 5) { if (q.done) break; plane(integral_constant<int, (KA > 5 ? 5 : 0)>{}); }
         }
         if (lane == 0) bulk_wait0();  // the output rows are written before the CTA exits
         if constexpr (TMR) {
