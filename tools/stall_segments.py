@@ -1,15 +1,18 @@
 """Warp-stall samples of an ncu SASS source page (--page source --csv
 --print-source sass), summed between synchronisation landmarks (development aid).
-usage: python tools/stall_segments.py full.sass.csv [min_exec]"""
+usage: python tools/stall_segments.py full.sass.csv [min_exec] [kernel section index]"""
 import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 minex = float(sys.argv[2]) if len(sys.argv) > 2 else 1000
-hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
+heads = [i for i, r in enumerate(rows) if r and r[0] == "Address"]
+sec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+hi = heads[sec]
+end = heads[sec + 1] - 1 if sec + 1 < len(heads) else len(rows)
 hdr = rows[hi]
 ix = {k: i for i, k in enumerate(hdr)}
-body = [r for r in rows[hi + 1:] if len(r) == len(hdr) and r[0].startswith("0x")]
+body = [r for r in rows[hi + 1:end] if len(r) == len(hdr) and r[0].startswith("0x")]
 allk = "Warp Stall Sampling (All Samples)"
 tot = sum(float(r[ix[allk]] or 0) for r in body)
 print("total samples", tot, "instructions", len(body))
