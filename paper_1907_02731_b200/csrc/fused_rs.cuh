@@ -20,10 +20,12 @@
 //
 // Roles (one 512-thread CTA per SM, persistent over (64 x 32 tile, frame
 // range) segments): 8 A warps issue the halo-box TMA loads (box b of a plane
-// by lane 0 of warp 6 + b) and run the x-pass; 8 B warps run the y-pass into
-// a ring of the last 2RT+1 y-filtered planes (registers, or tensor memory
-// for RT >= 3), the t-pass, the recombination, the store and the canonical
-// reductions. A and B meet at two mbarrier pairs per x-pass buffer.
+// by lane 0 of warp 6 + b) and run the x-pass; 8 B warps run the y-pass, the
+// t-pass (register variants: 2RT pending outputs kept as running sums, each
+// y-filtered plane scattered into them; RT >= 3: a ring of the last 2RT+1
+// planes in tensor memory, gathered at emission), the recombination, the
+// store and the canonical reductions. A and B meet at two mbarrier pairs per
+// x-pass buffer.
 #pragma once
 
 #include <type_traits>
