@@ -628,6 +628,20 @@ def main():
             other = {"arith": oth, "value": prob.voxels() * iters * 2 / (o_ms * 1e-3),
                      "ms_per_step": o_ms / 2, "kernel": kernel_name(c2, Cn, oth),
                      "hbm_frac": o_rl["hbm"]["frac"], "fp32_frac": o_rl["fp32"]["frac"]}
+        # opt-in FAST tap trimming (sfseg_ctx_set_tap_trim): an extra key, never
+        # the headline; reported only where it changes the kernel's support
+        if not args.no_extras and args.arith == "fast":
+            eff = list(gpu.E.effective_radii(cfg))
+            if eff != [int(r) for r in cfg.kernel.radii]:
+                gpu.ctx.set_tap_trim(True)
+                t_ms, t_f, t_lpi = gpu.timed_solves(cfg, 2, 1)
+                gpu.ctx.set_tap_trim(False)
+                line_extra["tap_trim"] = {
+                    "note": "opt-in (sfseg_ctx_set_tap_trim / SFSEG_FAST_TRIM=1), off in every other "
+                            "number of this line: taps at most 2^-24 of their axis's largest tap dropped",
+                    "effective_radii": eff, "value": prob.voxels() * iters * 2 / (t_ms * 1e-3),
+                    "ms_per_step": t_ms / 2, "fused_ms_per_iteration": t_f,
+                    "launches_per_iteration": t_lpi}
         # end to end through sfseg_run from pinned host memory
         soft = torch.empty((T, H, W), dtype=torch.float32, pin_memory=True)
         mask = torch.empty((T, H, W), dtype=torch.uint8, pin_memory=True)

@@ -134,6 +134,15 @@ int sfseg_ctx_destroy(sfseg_ctx* ctx);
 /* Enables per-launch CUDA-event timing of the stencil kernel (bench only). */
 int sfseg_ctx_set_timing(sfseg_ctx* ctx, int enabled);
 int sfseg_ctx_get_timing(const sfseg_ctx* ctx, sfseg_timing* out);
+/* FAST arithmetic only, off by default (SFSEG_FAST_TRIM=1 turns it on for new
+ * contexts): the outermost taps of an axis that are at most 2^-24 of the
+ * axis's largest tap are dropped symmetrically (they move an fp32 sum by less
+ * than half an ulp of its largest term) and the step runs the kernel of the
+ * remaining support; make_gaussian_kernel's taps (conv3d.cpp:23-58) are not
+ * renormalised. EXACT never trims. sfseg_effective_radii reports the radii a
+ * trimmed step would run (equal to p->radii when nothing is dropped). */
+int sfseg_ctx_set_tap_trim(sfseg_ctx* ctx, int enabled);
+int sfseg_effective_radii(const sfseg_params* p, int32_t out[3]);
 /* Blocks until the context stream is idle. */
 int sfseg_ctx_synchronize(sfseg_ctx* ctx);
 /* Sum of the fused-step kernel times (CUDA events on the context stream)

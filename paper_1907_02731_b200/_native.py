@@ -170,6 +170,8 @@ _SIGS = {
     "sfseg_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "sfseg_ctx_destroy": (C.c_int, [_P]),
     "sfseg_ctx_set_timing": (C.c_int, [_P, C.c_int]),
+    "sfseg_ctx_set_tap_trim": (C.c_int, [_P, C.c_int]),
+    "sfseg_effective_radii": (C.c_int, [C.POINTER(Params), C.POINTER(C.c_int32)]),
     "sfseg_ctx_get_timing": (C.c_int, [_P, C.POINTER(Timing)]),
     "sfseg_ctx_synchronize": (C.c_int, [_P]),
     "sfseg_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),

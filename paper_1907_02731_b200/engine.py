@@ -190,6 +190,12 @@ class Context:
     def set_timing(self, on: bool) -> None:
         N.check(self._lib.sfseg_ctx_set_timing(self.handle, int(on)))
 
+    def set_tap_trim(self, on: bool) -> None:
+        """FAST arithmetic only, off by default: drop the outermost taps that
+        are at most 2^-24 of their axis's largest tap and run the kernel of the
+        remaining support (sfseg_ctx_set_tap_trim, include/sfseg_cuda.h)."""
+        N.check(self._lib.sfseg_ctx_set_tap_trim(self.handle, int(on)))
+
     def timing(self) -> N.Timing:
         t = N.Timing()
         N.check(self._lib.sfseg_ctx_get_timing(self.handle, C.byref(t)))
@@ -269,6 +275,15 @@ def _same_mem(bufs: Sequence[_Buf]) -> int:
 
 
 # ---------------------------------------------------------------------------
+def effective_radii(cfg: "SfsegConfig") -> tuple:
+    """Radii a tap-trimmed FAST step runs for cfg's kernel (Context.set_tap_trim);
+    equal to cfg's radii when every tap is above fp32 resolution."""
+    out = (C.c_int32 * 3)()
+    q = cfg.to_params()
+    N.check(N.load_library().sfseg_effective_radii(C.byref(q), out))
+    return tuple(int(v) for v in out)
+
+
 def make_gaussian_kernel(sigmas, radii) -> SeparableKernel3D:
     """make_gaussian_kernel (conv3d.cpp:40-58); fp64 taps, mass folded into taps_t."""
     lib = N.load_library()

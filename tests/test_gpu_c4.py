@@ -80,6 +80,49 @@ def test_c4_crop_checkpoints_match_reference(c4_crop, arith):
     assert np.allclose(mine, norms, rtol=1e-9 if arith == "exact" else 1e-5)
 
 
+def test_c4_crop_tap_trim_matches_reference(c4_crop):
+    # opt-in FAST tap trimming (sfseg_ctx_set_tap_trim): c4's taps beyond
+    # |d| = 8 (space) and |d| = 2 (time) are below 2^-24 of the centre tap, the
+    # step runs as (2, 8, 8); same gates against the reference at every
+    # checkpoint, and fp32-rounding-level distance from the untrimmed solve
+    prob, fs, want, snaps, norms = c4_crop
+    iters = prob.cfg.iterations
+    cfg = _cfg(prob, "fast", iterations=iters, binarize_start=iters + 1)
+    assert E.effective_radii(cfg) == (2, 8, 8)
+    for i in (0, 1, 2, 3):  # the other BASELINE kernels keep every tap
+        other = synth.config(i)[0].cfg
+        assert E.effective_radii(other) == tuple(other.kernel.radii)
+    ctx = E.Context(0)
+    try:
+        ctx.set_tap_trim(True)
+        got = {}
+        res = E.run(fs, cfg, ctx=ctx,
+                    observer=lambda it, x: got.__setitem__(it, x.copy()) if it in CKS else None)
+    finally:
+        ctx.close()
+    for it in CKS:
+        gates(got[it], snaps[it], cfg.final_threshold, f"c4 crop trimmed iter {it}")
+    gates(res.soft, want, cfg.final_threshold, "c4 crop trimmed final")
+    mine = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
+    assert np.allclose(mine, norms, rtol=1e-5)
+    base = E.run(fs, cfg)
+    d = float(np.max(np.abs(res.soft.astype(np.float64) - base.soft)))
+    assert d <= 1e-5 * float(base.soft.max()), d
+    assert not np.array_equal(res.soft, base.soft)  # the trimmed kernel did run
+    # EXACT never trims: bit-identical with the switch on
+    ctx = E.Context(0)
+    try:
+        ctx.set_tap_trim(True)
+        small = synth.config(4, frames=6)[0]
+        sf, _ = small.generate()
+        ecfg = _cfg(small, "exact", iterations=2, binarize_start=3)
+        a = E.run(sf, ecfg, ctx=ctx)
+    finally:
+        ctx.close()
+    b = E.run(sf, ecfg)
+    assert np.array_equal(a.soft, b.soft)
+
+
 @pytest.mark.parametrize("arith", ["fast", "exact"])
 def test_c4_crop_run_once_matches_run(c4_crop, arith):
     # sfseg_run in one call equals the load/solve/download sequence bit for bit
