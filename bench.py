@@ -176,7 +176,8 @@ def bytes_per_voxel(channels: int) -> int:
 def kernel_name(cfg, channels: int, arith: str) -> str:
     rt, r = cfg.kernel.radii[0], max(cfg.kernel.radii[1:])
     if arith == "fast" and channels > 1:
-        return (f"fused_step_mc<RT={rt},R={r}> HEAD(u, Q u, f_1 u) + {channels // 2} TAIL "
+        head = "HEAD(u, Q u, f_1 u)" if channels % 2 else "HEAD(u, Q u)"
+        return (f"fused_step_mc<RT={rt},R={r}> {head} + {channels // 2} TAIL "
                 f"launch(es) per iteration (FAST, (C+2)-field form)")
     if arith == "fast":
         return f"fused_step_rs<RT={rt},R={r}> (FAST)"

@@ -20,7 +20,9 @@
 //   TAIL (later launches, NF = 1 or 2): raw boxes U, f_a [, f_b]; fields
 //        f_a u [, f_b u]; y += 2 S^p (f_a G(f_a u) + f_b G(f_b u))
 //
-// c4 (C = 3) is HEAD(3) + TAIL(2): two passes per iteration.
+// c4 (C = 3) is HEAD(3) + TAIL(2): two passes per iteration. An even channel
+// count runs HEAD(2) + C/2 TAIL(2) (c2, C = 8: five passes, none of them a
+// one-channel TAIL).
 //
 // U = S^p x is the u field itself. The last launch of a step writes, instead
 // of y_{k+1}, U_{k+1} = S^p y_{k+1} (write_u) whenever the next iteration

@@ -328,10 +328,13 @@ FusedVariant variant_rs() {
 struct McVariant {
     int rt, r;
     int threads, box_w, box_h;
-    size_t smem[4];          // head, tail of 2 channels, tail of 1, EXACT per channel
-    void (*kernel[4])(FusedArgs);
+    size_t smem[5];          // head (u, Q u, f_1 u), tail of 2 channels, tail of 1, EXACT per channel, head (u, Q u)
+    void (*kernel[5])(FusedArgs);
 };
-constexpr int kHeadChannels = 1;  // channels folded into the HEAD launch (f_1 u)
+// channels folded into the HEAD launch: f_1 for an odd channel count (c4:
+// HEAD(3) + one TAIL(2)); none for an even one, where the same number of
+// launches then needs no one-channel TAIL (c2: HEAD(2) + four TAIL(2))
+constexpr int head_channels(int C) { return C % 2; }
 
 template <int RT, int R>
 McVariant variant_mc() {
@@ -342,6 +345,7 @@ McVariant variant_mc() {
     using G2 = sfk::McGeom<RT, R, 2, sfk::MC_TAIL>;
     using G1 = sfk::McGeom<RT, R, 1, sfk::MC_TAIL>;
     using GE = sfk::McGeom<RT, R, 3, sfk::MC_EXACT>;
+    using GH2 = sfk::McGeom<RT, R, 2, sfk::MC_HEAD>;
     v.threads = GH::NT;
     v.box_w = GH::BW;
     v.box_h = GH::BH;
@@ -353,6 +357,8 @@ McVariant variant_mc() {
     v.kernel[1] = sfk::fused_step_mc<RT, R, 2, sfk::MC_TAIL>;
     v.kernel[2] = sfk::fused_step_mc<RT, R, 1, sfk::MC_TAIL>;
     v.kernel[3] = sfk::fused_step_mc<RT, R, 3, sfk::MC_EXACT>;
+    v.smem[4] = GH2::SMEM_BYTES;
+    v.kernel[4] = sfk::fused_step_mc<RT, R, 2, sfk::MC_HEAD>;
     return v;
 }
 
@@ -1072,9 +1078,10 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
     upload_schedule(c, a.tiles_x * a.tiles_y, c->Tout(), grid_n);
     a.sched = c->sched_seg;
     a.sched_off = c->sched_off;
-    for (int i = 0; i < 4; ++i) ensure_smem_attr(c, v.kernel[i], v.smem[i]);
+    for (int i = 0; i < 5; ++i) ensure_smem_attr(c, v.kernel[i], v.smem[i]);
     const int C = static_cast<int>(Fch.size());
-    const int ntail = exact ? C - 1 : (C - kHeadChannels + 1) / 2;
+    const int hc = head_channels(C);
+    const int ntail = exact ? C - 1 : (C - hc + 1) / 2;
     for (int g = 0; g <= ntail; ++g) {
         int kind = 0;
         if (exact) {  // one launch per channel: boxes x, S^p, f_g; operands S^p, f_g, y
@@ -1082,14 +1089,17 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
             a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, fv.tx, 8);
-        } else if (g == 0) {  // boxes U, Q, f_1; operands S^p, Q, f_1
+        } else if (g == 0) {  // boxes U, Q [, f_1]; operands S^p, Q [, f_1]
+            kind = hc ? 0 : 4;
             a.tm_x = make_tmap(u, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(q, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(q, c->T, c->H, c->W, c->P, fv.tx, 8);
-            a.tm_f[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
-            a.tm_fc[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, fv.tx, 8);
+            if (hc) {
+                a.tm_f[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
+                a.tm_fc[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, fv.tx, 8);
+            }
         } else {  // boxes U, f_a [, f_b]; operands S^p, f_a [, f_b], y
-            const int c0 = kHeadChannels + 2 * (g - 1), n = std::min(2, C - c0);
+            const int c0 = hc + 2 * (g - 1), n = std::min(2, C - c0);
             kind = n == 2 ? 1 : 2;
             for (int i = 0; i < n; ++i) {
                 a.tm_f[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
