@@ -17,7 +17,7 @@
 //
 //   HEAD (first launch, NF = 2 or 3): raw boxes U, Q [, f_1]; fields u, Q u
 //        [, f_1 u]; y = S^p ((C/alpha - Q) G(u) - G(Q u) [+ 2 f_1 G(f_1 u)])
-//   TAIL (later launches, NF = 1 or 2): raw boxes U, f_a [, f_b]; fields
+//   TAIL (later launches, NF = 2; NF = 1 compiles but no grouping needs it): raw boxes U, f_a [, f_b]; fields
 //        f_a u [, f_b u]; y += 2 S^p (f_a G(f_a u) + f_b G(f_b u))
 //
 // c4 (C = 3) is HEAD(3) + TAIL(2): two passes per iteration. An even channel

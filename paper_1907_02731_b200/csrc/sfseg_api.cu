@@ -328,8 +328,8 @@ FusedVariant variant_rs() {
 struct McVariant {
     int rt, r;
     int threads, box_w, box_h;
-    size_t smem[5];          // head (u, Q u, f_1 u), tail of 2 channels, tail of 1, EXACT per channel, head (u, Q u)
-    void (*kernel[5])(FusedArgs);
+    size_t smem[4];          // head (u, Q u, f_1 u), tail of 2 channels, EXACT per channel, head (u, Q u)
+    void (*kernel[4])(FusedArgs);
 };
 // channels folded into the HEAD launch: f_1 for an odd channel count (c4:
 // HEAD(3) + one TAIL(2)); none for an even one, where the same number of
@@ -343,7 +343,6 @@ McVariant variant_mc() {
     v.r = R;
     using GH = sfk::McGeom<RT, R, 3, sfk::MC_HEAD>;
     using G2 = sfk::McGeom<RT, R, 2, sfk::MC_TAIL>;
-    using G1 = sfk::McGeom<RT, R, 1, sfk::MC_TAIL>;
     using GE = sfk::McGeom<RT, R, 3, sfk::MC_EXACT>;
     using GH2 = sfk::McGeom<RT, R, 2, sfk::MC_HEAD>;
     v.threads = GH::NT;
@@ -351,14 +350,12 @@ McVariant variant_mc() {
     v.box_h = GH::BH;
     v.smem[0] = GH::SMEM_BYTES;
     v.smem[1] = G2::SMEM_BYTES;
-    v.smem[2] = G1::SMEM_BYTES;
-    v.smem[3] = GE::SMEM_BYTES;
+    v.smem[2] = GE::SMEM_BYTES;
     v.kernel[0] = sfk::fused_step_mc<RT, R, 3, sfk::MC_HEAD>;
     v.kernel[1] = sfk::fused_step_mc<RT, R, 2, sfk::MC_TAIL>;
-    v.kernel[2] = sfk::fused_step_mc<RT, R, 1, sfk::MC_TAIL>;
-    v.kernel[3] = sfk::fused_step_mc<RT, R, 3, sfk::MC_EXACT>;
-    v.smem[4] = GH2::SMEM_BYTES;
-    v.kernel[4] = sfk::fused_step_mc<RT, R, 2, sfk::MC_HEAD>;
+    v.kernel[2] = sfk::fused_step_mc<RT, R, 3, sfk::MC_EXACT>;
+    v.smem[3] = GH2::SMEM_BYTES;
+    v.kernel[3] = sfk::fused_step_mc<RT, R, 2, sfk::MC_HEAD>;
     return v;
 }
 
@@ -1078,19 +1075,19 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
     upload_schedule(c, a.tiles_x * a.tiles_y, c->Tout(), grid_n);
     a.sched = c->sched_seg;
     a.sched_off = c->sched_off;
-    for (int i = 0; i < 5; ++i) ensure_smem_attr(c, v.kernel[i], v.smem[i]);
+    for (int i = 0; i < 4; ++i) ensure_smem_attr(c, v.kernel[i], v.smem[i]);
     const int C = static_cast<int>(Fch.size());
     const int hc = head_channels(C);
     const int ntail = exact ? C - 1 : (C - hc + 1) / 2;
     for (int g = 0; g <= ntail; ++g) {
         int kind = 0;
         if (exact) {  // one launch per channel: boxes x, S^p, f_g; operands S^p, f_g, y
-            kind = 3;
+            kind = 2;
             a.tm_x = make_tmap(x_src, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(Fch[g], c->T, c->H, c->W, c->P, fv.tx, 8);
         } else if (g == 0) {  // boxes U, Q [, f_1]; operands S^p, Q [, f_1]
-            kind = hc ? 0 : 4;
+            kind = hc ? 0 : 3;
             a.tm_x = make_tmap(u, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_f[0] = make_tmap(q, c->T, c->H, c->W, c->P, v.box_w, v.box_h);
             a.tm_fc[0] = make_tmap(q, c->T, c->H, c->W, c->P, fv.tx, 8);
@@ -1098,9 +1095,9 @@ void launch_step_mc(sfseg_ctx* c, const HostKernel& k, double alpha, const float
                 a.tm_f[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
                 a.tm_fc[1] = make_tmap(Fch[0], c->T, c->H, c->W, c->P, fv.tx, 8);
             }
-        } else {  // boxes U, f_a [, f_b]; operands S^p, f_a [, f_b], y
-            const int c0 = hc + 2 * (g - 1), n = std::min(2, C - c0);
-            kind = n == 2 ? 1 : 2;
+        } else {  // boxes U, f_a, f_b; operands S^p, f_a, f_b, y (C - hc is even: always two channels)
+            const int c0 = hc + 2 * (g - 1), n = 2;
+            kind = 1;
             for (int i = 0; i < n; ++i) {
                 a.tm_f[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, v.box_w, v.box_h);
                 a.tm_fc[i] = make_tmap(Fch[c0 + i], c->T, c->H, c->W, c->P, fv.tx, 8);
