@@ -105,7 +105,12 @@ def test_c4_crop_tap_trim_matches_reference(c4_crop):
     gates(res.soft, want, cfg.final_threshold, "c4 crop trimmed final")
     mine = np.array([r.l2_norm_pre_normalize for r in res.trace.iterations])
     assert np.allclose(mine, norms, rtol=1e-5)
-    base = E.run(fs, cfg)
+    ctx = E.Context(0)
+    try:
+        ctx.set_tap_trim(False)  # whatever SFSEG_FAST_TRIM says
+        base = E.run(fs, cfg, ctx=ctx)
+    finally:
+        ctx.close()
     d = float(np.max(np.abs(res.soft.astype(np.float64) - base.soft)))
     assert d <= 1e-5 * float(base.soft.max()), d
     assert not np.array_equal(res.soft, base.soft)  # the trimmed kernel did run
